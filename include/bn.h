@@ -1,0 +1,131 @@
+/*
+ * bn.h — C ABI of the B200-native batched midsize-integer library (libbn.so).
+ *
+ * Implements the data-parallel hot path of Oancea & Watt, "GPU
+ * Implementations for Midsize Integer Addition and Multiplication"
+ * (arXiv 2405.14642; PAPER.md = /root/reference/PAPER.md at build time):
+ * batches of fixed-width unsigned integers, one instance (or a few) per CTA,
+ * sm_100a only.  No CUDA or torch types appear in the signatures.
+ *
+ * REPRESENTATION (§2): an integer is M little-endian limbs
+ * A = sum_i a_i x^i, x = 2^(limb_bits); "the result has the same length and
+ * element type as the input integers".  A batch is instance-major and
+ * contiguous: instance k occupies limbs [k*n_limbs, (k+1)*n_limbs).
+ * limb_bits = 64 is accepted and is the same bytes as 2*n_limbs u32 limbs
+ * (little-endian device), so every kernel works on u32 limbs internally.
+ *
+ * SIZES: bits = n_limbs * limb_bits must be a power of two in
+ * [1024, 262144] (the paper's 2^11..2^18 sweep, PAPER.md:919 and Tables 1-2,
+ * plus 2^10).  262144 bits is the largest size whose exact NTT product fits
+ * one CTA's shared memory (DESIGN.md §Data layout).
+ *
+ * POINTERS: a, b, out are DEVICE pointers on the current CUDA device, 16-byte
+ * aligned.  out may equal a or b exactly (in-place); a partial overlap is
+ * rejected.  The caller owns every buffer; the library owns only immutable
+ * per-device NTT constant tables (freed at process exit).
+ *
+ * STREAMS: every call is stream-ordered and asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default stream), performs no allocation and
+ * no host synchronisation (bn_prepare excepted).
+ *
+ * ERRORS: argument errors return synchronously before any launch and write
+ * nothing; a failed launch returns BN_ECUDA (see bn_cuda_error()); device
+ * faults surface at the caller's next synchronisation.  n_inst == 0 returns
+ * BN_OK without launching.
+ */
+#ifndef BN_H_
+#define BN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *bn_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    BN_OK = 0,
+    BN_EINVAL = 1, /* NULL pointer, limb_bits not 32/64, n_limbs == 0, bad op */
+    BN_ESIZE = 2,  /* n_limbs*limb_bits not a power of two in [1024, 262144] */
+    BN_EALIGN = 3, /* a, b or out not 16-byte aligned */
+    BN_EALIAS = 4, /* out partially overlaps a or b (exact equality allowed) */
+    BN_ECUDA = 5,  /* CUDA launch / configuration / copy failure */
+    BN_ENODEV = 6  /* no usable sm_100 device */
+} bn_status;
+
+/*
+ * bn_add — out[k] = (a[k] + b[k]) mod 2^bits, k in [0, n_inst).
+ * PAPER.md:144-163 (§2: map -> exclusive carry scan -> map), the carry
+ * operator of PAPER.md:177-205 / Fig. 3 (carry_op_eff), batched as bbadd
+ * (PAPER.md:232-234).  Each instance's carry-in is zero and its top carry-out
+ * is dropped (fixed width; reading R1/R4).
+ */
+bn_status bn_add(void *out, const void *a, const void *b, uint64_t n_inst,
+                 uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
+
+/*
+ * bn_mul_classical — out[k] = (a[k] * b[k]) mod 2^bits by the quadratic
+ * algorithm: Eq. (1) with the load-balanced result
+ * partitioning of Fig. 5, per-thread convolution and
+ * L/H publish of Figs. 6-7, carries resolved by the
+ * addition above.
+ */
+bn_status bn_mul_classical(void *out, const void *a, const void *b, uint64_t n_inst,
+                           uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
+
+/*
+ * bn_mul_ntt — out[k] = (a[k] * b[k]) mod 2^bits by number-theoretic
+ * transform over word-size primes p = k*2^n + 1 (§4).
+ * Exact variant (readings R10/R11): 32-bit limbs are the digits,
+ * zero-padded to N = 2*n_limbs32 points, three primes < 2^30 and Garner CRT,
+ * Shoup/Montgomery modular arithmetic ("further improvement
+ * would be expected using Montgomery representation").  Results are
+ * bit-identical to bn_mul_classical.  Builds the constant tables on first use
+ * on a device (bn_prepare), which synchronises once.
+ */
+bn_status bn_mul_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
+                     uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
+
+/* Build the NTT twiddle/CRT tables for `device` (all sizes), synchronously.
+ * Idempotent and thread-safe; bn_mul_ntt calls it lazily. */
+bn_status bn_prepare(int device);
+
+/* ---- host-buffer entry point (end-to-end path) ---------------------------
+ * bn_run_host — runs a sequence of operations over HOST operands: the batch
+ * is cut into chunks that are copied host->device, processed by each op in
+ * `ops` (same operands a, b), and copied device->host into outs[i], with
+ * copies and kernels overlapped on two streams of the current device.
+ * ops[i] is one of BN_OP_ADD / BN_OP_MUL_CLASSICAL / BN_OP_MUL_NTT;
+ * outs[i] is a host buffer of n_inst*n_limbs limbs.  Host buffers should be
+ * page-locked (cudaHostAlloc / torch pin_memory) for full bandwidth.
+ * Device scratch is allocated on first use and cached per device (grown on
+ * demand).  Synchronous: returns when every output is in host memory. */
+enum { BN_OP_ADD = 0, BN_OP_MUL_CLASSICAL = 1, BN_OP_MUL_NTT = 2 };
+bn_status bn_run_host(const int *ops, void *const *outs, int n_ops, const void *a,
+                      const void *b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
+
+/* ---- introspection ------------------------------------------------------ */
+uint32_t bn_max_bits(void);                /* 262144 */
+uint32_t bn_min_bits(void);                /* 1024 */
+int bn_cuda_error(void);                   /* last cudaError_t seen by this thread */
+const char *bn_status_string(bn_status s); /* static string */
+/* Number of kernel launches one call of `op` makes at this size (>= 1), for
+ * launch accounting in the benchmark; 0 for an unsupported size/op. */
+uint32_t bn_launches_per_call(int op, uint32_t bits);
+
+/* ---- NTT introspection / debug (tests only; not on the hot path) --------
+ * bn_ntt_primes — writes the three primes used by bn_mul_ntt to p[0..2].
+ * bn_debug_ntt_forward — x (device, n_inst*N u32 residues < p) -> forward
+ * transform of each length-N row over prime index `prime` (0..2), in place,
+ * output in BIT-REVERSED order and in [0, p), with omega_N = the library's
+ * primitive N-th root for that prime, written to *omega_out.  N = 2^lg_n,
+ * lg_n in [6, 14]. */
+void bn_ntt_primes(uint32_t p[3]);
+bn_status bn_debug_ntt_forward(uint32_t *x, uint64_t n_inst, uint32_t lg_n, int prime,
+                               uint32_t *omega_out, bn_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BN_H_ */

@@ -1,0 +1,192 @@
+"""Thin Python binding over libbn.so (include/bn.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this
+module only checks tensor metadata, passes ``data_ptr()`` and the current
+CUDA stream, and maps status codes to exceptions.  There is NO CPU fallback:
+if the extension is missing or no CUDA device is present, calls raise.
+
+Tensors: ``torch.int32``/``torch.uint32`` (u32 limbs) or ``torch.int64``/
+``torch.uint64`` (u64 limbs), shape ``[n_inst, n_limbs]``, contiguous, on a
+CUDA device.  Bit patterns are the limbs, little-endian.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libbn.so")
+_lock = threading.Lock()
+_lib = None
+
+SUPPORTED_BITS = tuple(1 << k for k in range(10, 19))
+
+_STATUS = {0: "BN_OK", 1: "BN_EINVAL", 2: "BN_ESIZE", 3: "BN_EALIGN", 4: "BN_EALIAS",
+           5: "BN_ECUDA", 6: "BN_ENODEV"}
+
+OP_ADD, OP_MUL_CLASSICAL, OP_MUL_NTT = 0, 1, 2
+OPS = {"add": OP_ADD, "mul_classical": OP_MUL_CLASSICAL, "mul_ntt": OP_MUL_NTT}
+
+
+class BnError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        extra = ""
+        if status == 5 and _lib is not None:
+            extra = " (cudaError %d)" % _lib.bn_cuda_error()
+        super().__init__("%s: %s%s" % (where, _STATUS.get(status, str(status)), extra))
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libbn.so (built by __graft_entry__.build()); raise if missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_LIB_PATH):
+                raise ImportError("libbn.so not built at %s — run __graft_entry__.build()" % _LIB_PATH)
+            lib = ctypes.CDLL(_LIB_PATH)
+            vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
+            for name in ("bn_add", "bn_mul_classical", "bn_mul_ntt"):
+                f = getattr(lib, name)
+                f.argtypes = [vp, vp, vp, u64, u32, u32, vp]
+                f.restype = ctypes.c_int
+            lib.bn_prepare.argtypes = [ctypes.c_int]
+            lib.bn_prepare.restype = ctypes.c_int
+            lib.bn_run_host.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp), ctypes.c_int,
+                                        vp, vp, u64, u32, u32]
+            lib.bn_run_host.restype = ctypes.c_int
+            lib.bn_max_bits.restype = u32
+            lib.bn_min_bits.restype = u32
+            lib.bn_cuda_error.restype = ctypes.c_int
+            lib.bn_status_string.argtypes = [ctypes.c_int]
+            lib.bn_status_string.restype = ctypes.c_char_p
+            lib.bn_launches_per_call.argtypes = [ctypes.c_int, u32]
+            lib.bn_launches_per_call.restype = u32
+            lib.bn_ntt_primes.argtypes = [ctypes.POINTER(u32)]
+            lib.bn_ntt_primes.restype = None
+            lib.bn_debug_ntt_forward.argtypes = [vp, u64, u32, ctypes.c_int, ctypes.POINTER(u32), vp]
+            lib.bn_debug_ntt_forward.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def max_bits() -> int:
+    return int(load().bn_max_bits())
+
+
+def _limb_bits(t: torch.Tensor) -> int:
+    if t.dtype in (torch.int32, torch.uint32):
+        return 32
+    if t.dtype in (torch.int64, torch.uint64):
+        return 64
+    raise TypeError("limb tensors must be int32/uint32 or int64/uint64, got %s" % t.dtype)
+
+
+def _check(a: torch.Tensor, b: torch.Tensor, out):
+    if a.dim() != 2 or a.shape != b.shape:
+        raise ValueError("a and b must be [n_inst, n_limbs] with equal shapes")
+    if a.dtype != b.dtype:
+        raise TypeError("a and b must have the same dtype")
+    if not (a.is_cuda and b.is_cuda):
+        raise ValueError("operands must be CUDA tensors (no CPU fallback)")
+    if a.device != b.device:
+        raise ValueError("operands on different devices")
+    if not (a.is_contiguous() and b.is_contiguous()):
+        raise ValueError("operands must be contiguous")
+    if out is None:
+        out = torch.empty_like(a)
+    elif out.shape != a.shape or out.dtype != a.dtype or out.device != a.device or not out.is_contiguous():
+        raise ValueError("out must match a in shape, dtype, device and be contiguous")
+    return out
+
+
+def _call(name: str, a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    out = _check(a, b, out)
+    lib = load()
+    n_inst, n_limbs = a.shape
+    with torch.cuda.device(a.device):
+        stream = torch.cuda.current_stream(a.device).cuda_stream
+        st = getattr(lib, name)(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs,
+                                _limb_bits(a), stream)
+    if st != 0:
+        raise BnError(st, name)
+    return out
+
+
+def add(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    """(a + b) mod 2^bits per instance (bn_add)."""
+    return _call("bn_add", a, b, out)
+
+
+def mul_classical(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    """(a * b) mod 2^bits per instance, quadratic algorithm (bn_mul_classical)."""
+    return _call("bn_mul_classical", a, b, out)
+
+
+def mul_ntt(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    """(a * b) mod 2^bits per instance, exact 3-prime NTT (bn_mul_ntt)."""
+    return _call("bn_mul_ntt", a, b, out)
+
+
+def prepare(device: int = 0) -> None:
+    st = load().bn_prepare(device)
+    if st != 0:
+        raise BnError(st, "bn_prepare")
+
+
+def run_host(ops, a: torch.Tensor, b: torch.Tensor, outs=None):
+    """End-to-end path over HOST tensors (ideally pinned): bn_run_host.
+    ``ops`` is a list of names from OPS; returns the list of host outputs."""
+    if a.is_cuda or b.is_cuda:
+        raise ValueError("run_host takes host tensors")
+    if a.dim() != 2 or a.shape != b.shape or a.dtype != b.dtype:
+        raise ValueError("a and b must be [n_inst, n_limbs] with equal shapes and dtypes")
+    if not (a.is_contiguous() and b.is_contiguous()):
+        raise ValueError("operands must be contiguous")
+    codes = [OPS[o] for o in ops]
+    if outs is None:
+        outs = [torch.empty_like(a, pin_memory=a.is_pinned()) for _ in codes]
+    lib = load()
+    n = len(codes)
+    c_ops = (ctypes.c_int * n)(*codes)
+    c_outs = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+    st = lib.bn_run_host(c_ops, c_outs, n, a.data_ptr(), b.data_ptr(), a.shape[0], a.shape[1],
+                         _limb_bits(a))
+    if st != 0:
+        raise BnError(st, "bn_run_host")
+    return outs
+
+
+def ntt_primes():
+    arr = (ctypes.c_uint32 * 3)()
+    load().bn_ntt_primes(arr)
+    return [int(x) for x in arr]
+
+
+def debug_ntt_forward(x: torch.Tensor, prime: int):
+    """Forward NTT of each row of x (int32 residues, length N = 2^lg), in place,
+    bit-reversed output; returns (x, omega).  Test/debug entry point only."""
+    if x.dim() != 2 or not x.is_cuda or not x.is_contiguous() or x.dtype not in (torch.int32, torch.uint32):
+        raise ValueError("x must be a contiguous CUDA int32 [n, N] tensor")
+    n, N = x.shape
+    lg = N.bit_length() - 1
+    if 1 << lg != N:
+        raise ValueError("N must be a power of two")
+    om = ctypes.c_uint32()
+    with torch.cuda.device(x.device):
+        st = load().bn_debug_ntt_forward(x.data_ptr(), n, lg, prime, ctypes.byref(om),
+                                         torch.cuda.current_stream(x.device).cuda_stream)
+    if st != 0:
+        raise BnError(st, "bn_debug_ntt_forward")
+    return x, int(om.value)
+
+
+def launches_per_call(op: str, bits: int) -> int:
+    return int(load().bn_launches_per_call(OPS[op], bits))

@@ -1,0 +1,131 @@
+"""CPU model of the carry-scan algebra the add kernel uses — -m "not gpu".
+
+Pins the paper's operators (Figs. 2/3) and the warp-level
+ballot-add formulation used in csrc/bn_scan.cuh against sequential folds:
+
+* carry_op_nice / carry_op_eff /
+  carry_op_sgm: associativity, identity, eff == nice.
+* ballot-add: with G = generate mask, P = propagate mask, X = G|P,
+  carry-in mask = (X + G + c0) ^ X ^ G equals the exclusive scan of
+  carry_op_eff over lanes (all 3^8 patterns of 8 lanes + random 32-lane).
+* segment isolation (reading R1): clearing the (g, p) bits of the top lane of
+  every segment gives each segment carry-in 0, whereas the literal exclusive
+  segmented scan leaks the previous segment's carry.
+"""
+import itertools
+import random
+
+
+def carry_op_nice(x, y):
+    ov1, mx1 = x
+    ov2, mx2 = y
+    return ((ov1 and mx2) or ov2, mx1 and mx2)
+
+
+def carry_op_eff(c1, c2):
+    return (c1 & c2 & 2) | (((c1 & (c2 >> 1)) | c2) & 1)
+
+
+def carry_op_sgm(c1, c2):
+    if c2 & 4:
+        return c2
+    return carry_op_eff(c1, c2) | ((c1 | c2) & 4)
+
+
+def test_eff_equals_nice_and_identity():
+    for ov1, mx1, ov2, mx2 in itertools.product((0, 1), repeat=4):
+        n = carry_op_nice((bool(ov1), bool(mx1)), (bool(ov2), bool(mx2)))
+        e = carry_op_eff(ov1 | (mx1 << 1), ov2 | (mx2 << 1))
+        assert e == int(n[0]) | (int(n[1]) << 1)
+    for c in range(4):
+        assert carry_op_eff(2, c) == c and carry_op_eff(c, 2) == c
+    for c in range(8):
+        assert carry_op_sgm(2, c) == c or (c & 4)  # 2 is neutral up to the segment bit
+
+
+def test_associativity_exhaustive():
+    for a, b, c in itertools.product(range(4), repeat=3):
+        assert carry_op_eff(carry_op_eff(a, b), c) == carry_op_eff(a, carry_op_eff(b, c))
+    for a, b, c in itertools.product(range(8), repeat=3):
+        assert carry_op_sgm(carry_op_sgm(a, b), c) == carry_op_sgm(a, carry_op_sgm(b, c))
+
+
+def _excl_scan(op, e, xs):
+    out, acc = [], e
+    for x in xs:
+        out.append(acc)
+        acc = op(acc, x)
+    return out
+
+
+def _ballot_cin(gs, ps, c0, width):
+    """the kernel's formula: carry-in mask = (X + G + c0) ^ X ^ G, X = G|P."""
+    G = sum(g << i for i, g in enumerate(gs))
+    P = sum(p << i for i, p in enumerate(ps))
+    X = G | P
+    S = X + G + c0
+    cin = (S ^ X ^ G) & ((1 << width) - 1)
+    cout = (S >> width) & 1
+    return [(cin >> i) & 1 for i in range(width)], cout
+
+
+def _seq(gs, ps, c0):
+    cins, c = [], c0
+    for g, p in zip(gs, ps):
+        cins.append(c)
+        c = g | (p & c)
+    return cins, c
+
+
+def test_ballot_add_all_8_lane_patterns():
+    # kill / generate / propagate per lane (g and p exclusive, as for chunk sums)
+    for pat in itertools.product((0, 1, 2), repeat=8):
+        gs = [int(x == 1) for x in pat]
+        ps = [int(x == 2) for x in pat]
+        for c0 in (0, 1):
+            assert _ballot_cin(gs, ps, c0, 8) == _seq(gs, ps, c0)
+            # and equals the paper's exclusive scan of carry_op_eff (ov=g, mx=p)
+            if c0 == 0:
+                sc = _excl_scan(carry_op_eff, 2, [g | (p << 1) for g, p in zip(gs, ps)])
+                assert [s & 1 for s in sc] == _seq(gs, ps, 0)[0]
+
+
+def test_ballot_add_random_32_lane():
+    rng = random.Random(5)
+    for _ in range(20000):
+        pat = [rng.choice((0, 1, 2, 2, 2)) for _ in range(32)]
+        gs = [int(x == 1) for x in pat]
+        ps = [int(x == 2) for x in pat]
+        c0 = rng.randrange(2)
+        assert _ballot_cin(gs, ps, c0, 32) == _seq(gs, ps, c0)
+
+
+def test_segment_isolation():
+    """IPB = 4 segments of 8 lanes: top lane of each segment masked to kill."""
+    rng = random.Random(9)
+    seg = 8
+    for _ in range(5000):
+        pat = [rng.choice((0, 1, 2)) for _ in range(32)]
+        gs = [int(x == 1) for x in pat]
+        ps = [int(x == 2) for x in pat]
+        mg = [0 if i % seg == seg - 1 else g for i, g in enumerate(gs)]
+        mp = [0 if i % seg == seg - 1 else p for i, p in enumerate(ps)]
+        cins, _ = _ballot_cin(mg, mp, 0, 32)
+        for s in range(0, 32, seg):
+            want, _ = _seq(gs[s:s + seg], ps[s:s + seg], 0)
+            assert cins[s:s + seg] == want
+
+
+def test_literal_segmented_scan_leaks():
+    """Reading R1: Fig. 2's scan^exc carry_op_sgm 2 with the segment bit on
+    the head element passes the previous segment's carry into the head."""
+    # two instances of M=2 limbs: (all-ones + 1) then (0 + 0)
+    M, MAX = 2, 0xFFFFFFFF
+    a = [MAX, MAX, 0, 0]
+    b = [1, 0, 0, 0]
+    flags = []
+    for i, (x, y) in enumerate(zip(a, b)):
+        p = (x + y) & MAX
+        flags.append((4 if i % M == 0 else 0) | ((p == MAX) << 1) | int(p < x))
+    carries = _excl_scan(carry_op_sgm, 2, flags)
+    assert carries[2] & 1 == 1  # the carry of instance 0 leaks into instance 1
