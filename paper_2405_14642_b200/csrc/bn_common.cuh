@@ -1,0 +1,166 @@
+// bn_common.cuh — device building blocks shared by the three hot-path kernels.
+//
+//   * 128-bit global/shared vector moves,
+//   * the carry-propagation scan of §2: per-thread
+//     sequential fold over L limbs ("efficient sequentialization",
+//     PAPER.md:283-292), a warp-level scan done with two ballots and one
+//     integer add, and a CTA-level scan of warp aggregates through shared
+//     memory (the hierarchical thread/warp/block decomposition of
+//     PAPER.md:289-292).
+//
+// The scan computes the same exclusive scan as the paper's carry_op_eff
+// (Fig. 3) over the (ov, mx) = (generate, propagate) pairs
+// of each limb: for a chunk, g = carry out with carry-in 0 and p = "every
+// limb sum is 0xFFFFFFFF"; carry-out(cin) = g | (p & cin).  Over the lanes of
+// a warp with G = ballot(g), P = ballot(p), X = G|P, the carry into lane i is
+// bit i of (X + G + c0) ^ X ^ G: integer addition IS the carry-lookahead
+// network (tests/test_scan_model.py pins this against the sequential fold on
+// all 3^8 8-lane patterns).  Instances never exchange carries: the top lane of
+// each segment has its (g, p) cleared (reading R1: each instance's
+// carry-in is 0 and its top carry-out is dropped).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define BN_DEV __device__ __forceinline__
+
+namespace bn {
+
+// ---------------------------------------------------------------- vector I/O
+BN_DEV uint4 ldg_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+BN_DEV void stg_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+template <int L>
+BN_DEV void load_limbs(uint32_t (&r)[L], const uint32_t* src) {
+  static_assert(L % 4 == 0, "L must be a multiple of 4");
+#pragma unroll
+  for (int v = 0; v < L / 4; v++) {
+    uint4 x = ldg_stream(reinterpret_cast<const uint4*>(src) + v);
+    r[4 * v + 0] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+  }
+}
+template <int L>
+BN_DEV void store_limbs(uint32_t* dst, const uint32_t (&r)[L]) {
+#pragma unroll
+  for (int v = 0; v < L / 4; v++)
+    stg_stream(reinterpret_cast<uint4*>(dst) + v,
+               make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+}
+template <int L>
+BN_DEV void lds_limbs(uint32_t (&r)[L], const uint32_t* src) {
+#pragma unroll
+  for (int v = 0; v < L / 4; v++) {
+    uint4 x = reinterpret_cast<const uint4*>(src)[v];
+    r[4 * v + 0] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+  }
+}
+template <int L>
+BN_DEV void sts_limbs(uint32_t* dst, const uint32_t (&r)[L]) {
+#pragma unroll
+  for (int v = 0; v < L / 4; v++)
+    reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+}
+
+// ------------------------------------------------------------- carry scan
+
+// Mask with bit l set for every lane l that is the top lane of a TPI-lane
+// segment (TPI a power of two <= 32).
+template <int TPI>
+constexpr uint32_t seg_top_mask() {
+  uint32_t m = 0;
+  for (int l = TPI - 1; l < 32; l += TPI) m |= 1u << l;
+  return m;
+}
+
+// Thread-level map + fold (PAPER.md:150-157 step (1), carry_op over the
+// thread's L limbs).  s = x + y limb-wise; returns chunk (g, p).
+template <int L>
+BN_DEV void chunk_sum(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&s)[L], uint32_t& g,
+                      uint32_t& p) {
+  g = 0;
+  p = 1;
+#pragma unroll
+  for (int i = 0; i < L; i++) {
+    s[i] = x[i] + y[i];
+    uint32_t ov = s[i] < x[i];
+    uint32_t mx = s[i] == 0xFFFFFFFFu;
+    g = ov | (mx & g);
+    p &= mx;
+  }
+}
+
+// Step (3): ripple the chunk's carry-in through its limbs.
+template <int L>
+BN_DEV void chunk_apply(uint32_t (&s)[L], uint32_t cin) {
+#pragma unroll
+  for (int i = 0; i < L; i++) {
+    uint32_t r = s[i] + cin;
+    cin = cin & (s[i] == 0xFFFFFFFFu);
+    s[i] = r;
+  }
+}
+
+// Exclusive carry scan across the TPI threads of each instance (steps (2)).
+// Threads of one instance are consecutive (tid / TPI = instance slot).
+// Every thread of the CTA must call this (it may contain __syncthreads when
+// TPI > 32).  `agg` is shared scratch of >= blockDim.x / 32 words.
+// Returns this thread's carry-in.
+template <int TPI>
+BN_DEV uint32_t carry_scan(uint32_t g, uint32_t p, uint32_t* agg) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t G = __ballot_sync(0xFFFFFFFFu, g);
+  uint32_t P = __ballot_sync(0xFFFFFFFFu, p);
+  if constexpr (TPI < 32) {
+    constexpr uint32_t top = seg_top_mask<TPI>();
+    G &= ~top;
+    P &= ~top;
+    uint32_t X = G | P;
+    uint32_t cin = ((X + G) ^ X ^ G);
+    return (cin >> lane) & 1u;
+  } else {
+    constexpr int WPI = TPI / 32;  // warps per instance
+    uint32_t X = G | P;
+    // warp aggregate: carry out of bit 31 with warp carry-in 0, and all-propagate
+    uint64_t S = (uint64_t)X + G;
+    const uint32_t warp = threadIdx.x >> 5;
+    if constexpr (WPI > 1) {
+      if (lane == 0) agg[warp] = (uint32_t)(S >> 32) | ((P == 0xFFFFFFFFu) << 1);
+      __syncthreads();
+      const uint32_t w0 = warp - (warp % WPI);  // first warp of my instance
+      uint32_t a = lane < WPI ? agg[w0 + lane] : 0u;
+      uint32_t G2 = __ballot_sync(0xFFFFFFFFu, a & 1u);
+      uint32_t P2 = __ballot_sync(0xFFFFFFFFu, (a >> 1) & 1u);
+      uint32_t X2 = G2 | P2;
+      uint32_t c0 = (((X2 + G2) ^ X2 ^ G2) >> (warp % WPI)) & 1u;
+      uint32_t cin = (X + G + c0) ^ X ^ G;
+      return (cin >> lane) & 1u;
+    } else {
+      uint32_t cin = ((X + G) ^ X ^ G);
+      return (cin >> lane) & 1u;
+    }
+  }
+}
+
+// r = x + y over an instance whose L*TPI limbs are spread over TPI
+// consecutive threads (thread k holds limbs [k*L, (k+1)*L)); valid == false
+// threads contribute kill and their result is garbage (not stored).
+template <int L, int TPI>
+BN_DEV void add_regs(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&r)[L], bool valid,
+                     uint32_t* agg) {
+  uint32_t g, p;
+  chunk_sum<L>(x, y, r, g, p);
+  if (!valid) g = p = 0;
+  uint32_t cin = carry_scan<TPI>(g, p, agg);
+  chunk_apply<L>(r, cin);
+}
+
+}  // namespace bn

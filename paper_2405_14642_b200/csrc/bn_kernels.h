@@ -1,0 +1,56 @@
+// bn_kernels.h — internal interface between the host dispatcher (bn_api.cu)
+// and the kernel translation units.  Not part of the public C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bn {
+
+constexpr int kNumPrimes = 3;
+constexpr int kMinLogN = 6;   // N = 2m, m = 32 limbs (1024 bits)
+constexpr int kMaxLogN = 14;  // m = 8192 limbs (262144 bits)
+
+// Per-prime constants of the exact NTT product (host-computed in bn_api.cu).
+struct PrimeConst {
+  uint32_t p;      // prime, 2^29 < p < 2^30, p = k 2^e + 1 with e >= 14
+  uint32_t p2;     // 2p
+  uint32_t pinv;   // -p^-1 mod 2^32 (Montgomery)
+  uint32_t one_sh; // floor(2^32 / p): Shoup constant of w = 1 (input reduction)
+};
+
+// Garner CRT constants (p0 < p1 < p2), folded with the inverse-transform
+// normalisation K_j = 2^32 * N^-1 mod p_j (Montgomery R and 1/N).  Each
+// multiplier is a Shoup pair (w, floor(w 2^32 / p)).
+struct CrtConst {
+  uint32_t k0, k0_sh;          // mod p0: K0
+  uint32_t k1i, k1i_sh;        // mod p1: K1 * p0^-1
+  uint32_t i01, i01_sh;        // mod p1: p0^-1
+  uint32_t k2i, k2i_sh;        // mod p2: K2 * (p0 p1)^-1
+  uint32_t i012, i012_sh;      // mod p2: (p0 p1)^-1
+  uint32_t p0i012, p0i012_sh;  // mod p2: p0 (p0 p1)^-1
+  uint32_t p01_lo, p01_hi;     // p0 * p1 (< 2^60)
+};
+
+// Twiddle tables for one transform length N = 2^lg, contiguous: the table of
+// prime j and direction d (0 = forward omega, 1 = inverse omega^-1) starts at
+// tw + (2 j + d) (N - 1); inside it stage s occupies entries
+// [N - (N >> s), N - (N >> (s+1))) holding (w^(k 2^s), Shoup(w^(k 2^s))) for
+// k < N >> (s+1).
+struct NttTables {
+  const uint2* tw;
+  uint32_t omega[kNumPrimes];  // primitive N-th roots used (host side; debug/tests)
+};
+
+// prime constants + per-lg CRT constants -> __constant__ memory of the current device
+cudaError_t upload_prime_consts(const PrimeConst (&pc)[kNumPrimes], const CrtConst (&crt)[kMaxLogN + 1]);
+
+cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                       cudaStream_t st, int n_sm);
+cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                 uint64_t n_inst, cudaStream_t st, int n_sm);
+cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                           uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm);
+cudaError_t launch_ntt_forward_debug(int lgn, uint32_t* x, uint64_t n_inst, int prime,
+                                     const NttTables& tb, cudaStream_t st);
+
+}  // namespace bn

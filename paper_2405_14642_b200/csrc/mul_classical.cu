@@ -1,0 +1,228 @@
+// mul_classical.cu — bn_mul_classical: quadratic multiplication, truncated.
+//
+// C_k = sum_{i+j=k, 0<=i,j,k<M} A_i B_j  (Eq. 1), with the
+// paper's load-balanced result partitioning (Fig. 5): a
+// thread owns the Q-column chunk starting at k1 = Q*g AND its mirror chunk
+// starting at k1' = M - Q*(g+1), so every thread forms ~Q*(M+Q) partial
+// products.  Per chunk (Fig. 7 `convolution`) the Q column
+// sums are accumulated in registers as 96-bit (lo, hi, top) values; `combine`
+// folds them into Q low words + high + carry; the results
+// are published into shared arrays L and H (Fig. 6 step 3, PAPER.md:498-500;
+// layout = DESIGN.md reading R8) and resolved by one scan-add R = L + H
+// (reusing the §2 carry scan).
+//
+// B200 specifics:
+//  * the column update is a u32 mad.lo.cc / madc.hi.cc / addc chain, which
+//    ptxas lowers to one IMAD.WIDE.U32 (with carry-out predicate) plus half an
+//    IADD3.X per 32x32 partial product — the kernel is bound by IMAD.WIDE
+//    issue on the FMA pipe (32 lanes/clk/SM measured, profiles/r01_int_peak);
+//  * the B operand is consumed through a sliding register window: one
+//    128-bit shared load of B and one broadcast 128-bit load of A per Q x Q
+//    block of partial products (the paper's loop at PAPER.md:583-588 with the
+//    triangle of PAPER.md:589-592 absorbed by a zero chunk in front of B);
+//  * the two partitions run as two calls of the same uniform loop, and for
+//    small sizes I instances are interleaved across the lanes of a warp so
+//    that lanes of a warp have (nearly) the same trip count: divergence
+//    overhead (C-1)Q/(M+Q) with C = 32/I column groups per warp (<= 3%).
+#include "bn_common.cuh"
+#include "bn_kernels.h"
+
+namespace bn {
+
+BN_DEV void mac3(uint32_t& lo, uint32_t& hi, uint32_t& top, uint32_t a, uint32_t b) {
+  asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+      "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+      "addc.u32 %2, %2, 0;"
+      : "+r"(lo), "+r"(hi), "+r"(top)
+      : "r"(a), "r"(b));
+}
+
+template <int LOGM, int Q_>
+struct MulCCfg {
+  static constexpr int M = 1 << LOGM;
+  static constexpr int Q = Q_;
+  static constexpr int G = M / (2 * Q);  // column-group threads per instance
+  // instances interleaved across warp lanes (keeps trip counts uniform)
+  static constexpr int I = (512 / G) >= 32 ? 32 : ((512 / G) < 1 ? 1 : 512 / G);
+  static constexpr int SET_T = I * G;                         // threads per instance set
+  static constexpr int SETS = SET_T >= 512 ? 1 : 512 / SET_T;  // sets per CTA
+  static constexpr int T = SETS * SET_T;                       // threads per CTA
+  static constexpr int IPB = SETS * I;                         // instances per CTA
+  static constexpr int SA = M + 4;  // A stride: SA/4 odd -> broadcast A loads of <= 8 instances hit distinct banks
+  // B stride: Q zero words + M, padded so that SB/4 == BS (mod 8), which makes the
+  // 128-bit window loads of the 8 lanes (inst_lo, g) of a quarter-warp conflict-free
+  static constexpr int BS = I >= 8 ? 1 : 8 / I;
+  static constexpr int SB = M + Q + (((4 * BS - Q) % 32) + 32) % 32;
+  static constexpr int SMEM_WORDS = IPB * (SA + SB) + T / 32;
+  static constexpr int MINB = T >= 1024 ? 1 : 2048 / T / 2;    // target residency
+  static_assert(Q >= 2 && (Q % 4) == 0, "Q must be a multiple of 4 (>= 2 for the L/H layout)");
+  static_assert(G >= 1, "size too small for Q");
+};
+
+// Q column sums starting at column Q*j0 (Fig. 7 convolution + combine).
+// Ash: instance A (A[i] at Ash[i]); Bsh: instance B with B[x] at Bsh[x],
+// B[-Q..-1] == 0.
+template <int Q>
+BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_t (&lhcs)[Q + 2]) {
+  uint32_t lo[Q], hi[Q], top[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) lo[q] = hi[q] = top[q] = 0;
+  uint32_t cur[Q], prev[Q];
+  lds_limbs<Q>(cur, Bsh + Q * j0);
+#pragma unroll 1
+  for (int c = 0; c <= j0; c++) {
+    uint32_t av[Q];
+    lds_limbs<Q>(av, Ash + Q * c);
+    lds_limbs<Q>(prev, Bsh + Q * (j0 - c - 1));
+#pragma unroll
+    for (int s = 0; s < Q; s++) {
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const int d = q - s;
+        const uint32_t bj = d >= 0 ? cur[d] : prev[Q + d];
+        mac3(lo[q], hi[q], top[q], av[s], bj);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; q++) cur[q] = prev[q];
+  }
+  // combine: accum = (lo, hi), carry = top
+  lhcs[0] = lo[0];
+  uint32_t h_res = hi[0], c_res = top[0];
+#pragma unroll
+  for (int q = 1; q < Q; q++) {
+    const uint32_t l = lo[q], h = hi[q];
+    lhcs[q] = l + h_res;
+    h_res = h + (c_res + (lhcs[q] < l));
+    c_res = top[q] + (h_res < h);
+  }
+  lhcs[Q] = h_res;
+  lhcs[Q + 1] = c_res;
+}
+
+template <int LOGM, int Q>
+__global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
+    mul_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
+  using C = MulCCfg<LOGM, Q>;
+  constexpr int M = C::M;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* As = sm;                    // IPB * SA
+  uint32_t* Bs = sm + C::IPB * C::SA;   // IPB * SB  (B[x] at Bs[k*SB + Q + x])
+  uint32_t* agg = Bs + C::IPB * C::SB;  // T/32
+
+  const int t = threadIdx.x;
+  // convolution mapping: lane = inst_lo + I * g_lo (instance-fastest)
+  const int set = t / C::SET_T;
+  const int r = t % C::SET_T;
+  const int conv_slot = set * C::I + (r % C::I);
+  const int g = r / C::I;
+  // resolve/store mapping: instance-major, G consecutive threads per instance
+  const int add_slot = t / C::G;
+  const int chunk = t % C::G;
+
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t inst0 = grp * C::IPB;
+    // ---- stage A, B: coalesced 128-bit loads -> shared
+    constexpr int VPI = M / 4;  // uint4 per instance operand
+    for (int v = t; v < C::IPB * VPI; v += C::T) {
+      const int k = v / VPI, w = (v % VPI) * 4;
+      const uint64_t inst = inst0 + k;
+      uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
+      if (inst < n_inst) {
+        x = ldg_stream(reinterpret_cast<const uint4*>(a + inst * M + w));
+        y = ldg_stream(reinterpret_cast<const uint4*>(b + inst * M + w));
+      }
+      *reinterpret_cast<uint4*>(As + k * C::SA + w) = x;
+      *reinterpret_cast<uint4*>(Bs + k * C::SB + Q + w) = y;
+    }
+    for (int v = t; v < C::IPB * Q; v += C::T) Bs[(v / Q) * C::SB + (v % Q)] = 0u;  // B[-Q..-1]
+    __syncthreads();
+
+    // ---- convolution: low chunk j0 = g and mirror chunk j0' = M/Q - 1 - g
+    uint32_t lh0[Q + 2], lh1[Q + 2];
+    {
+      const uint32_t* Ai = As + conv_slot * C::SA;
+      const uint32_t* Bi = Bs + conv_slot * C::SB + Q;
+      conv_chunk<Q>(Ai, Bi, g, lh0);
+      conv_chunk<Q>(Ai, Bi, M / Q - 1 - g, lh1);
+    }
+    __syncthreads();
+
+    // ---- publish (reading R8): L[k1+q] = low_q; H[k1+Q] = high; H[k1+Q+1] = carry;
+    // H[k1+Q+2 .. k1+2Q) = 0; the top chunk zeroes H[0..Q) instead.
+    {
+      uint32_t* L = As + conv_slot * C::SA;
+      uint32_t* H = Bs + conv_slot * C::SB + Q;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t* lh = h == 0 ? lh0 : lh1;
+        const int j0 = h == 0 ? g : M / Q - 1 - g;
+        const int k1 = Q * j0;
+        uint32_t lows[Q], hs[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+          lows[q] = lh[q];
+          hs[q] = q == 0 ? lh[Q] : (q == 1 ? lh[Q + 1] : 0u);
+        }
+        sts_limbs<Q>(L + k1, lows);
+        if (k1 + Q < M) {
+          sts_limbs<Q>(H + k1 + Q, hs);
+        } else {
+          uint32_t z[Q];
+#pragma unroll
+          for (int q = 0; q < Q; q++) z[q] = 0;
+          sts_limbs<Q>(H, z);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- resolve R = L + H and store
+    {
+      constexpr int L2 = 2 * Q;
+      const uint64_t inst = inst0 + add_slot;
+      const bool valid = inst < n_inst;
+      uint32_t x[L2], y[L2], res[L2];
+      lds_limbs<L2>(x, As + add_slot * C::SA + L2 * chunk);
+      lds_limbs<L2>(y, Bs + add_slot * C::SB + Q + L2 * chunk);
+      add_regs<L2, C::G>(x, y, res, valid, agg);
+      if (valid) store_limbs<L2>(out + inst * M + L2 * chunk, res);
+    }
+    __syncthreads();  // smem reused by the next group
+  }
+}
+
+template <int LOGM>
+static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                 cudaStream_t st, int n_sm) {
+  constexpr int Q = 4;
+  using C = MulCCfg<LOGM, Q>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(mul_classical_kernel<LOGM, Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  const uint64_t cap = (uint64_t)n_sm * C::MINB * 16;
+  const unsigned grid = (unsigned)(n_groups < cap ? n_groups : cap);
+  mul_classical_kernel<LOGM, Q><<<grid, C::T, smem, st>>>(out, a, b, n_inst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                 uint64_t n_inst, cudaStream_t st, int n_sm) {
+  switch (logm) {
+    case 5: return launch_mulc_t<5>(out, a, b, n_inst, st, n_sm);
+    case 6: return launch_mulc_t<6>(out, a, b, n_inst, st, n_sm);
+    case 7: return launch_mulc_t<7>(out, a, b, n_inst, st, n_sm);
+    case 8: return launch_mulc_t<8>(out, a, b, n_inst, st, n_sm);
+    case 9: return launch_mulc_t<9>(out, a, b, n_inst, st, n_sm);
+    case 10: return launch_mulc_t<10>(out, a, b, n_inst, st, n_sm);
+    case 11: return launch_mulc_t<11>(out, a, b, n_inst, st, n_sm);
+    case 12: return launch_mulc_t<12>(out, a, b, n_inst, st, n_sm);
+    case 13: return launch_mulc_t<13>(out, a, b, n_inst, st, n_sm);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace bn

@@ -1,0 +1,417 @@
+// mul_ntt.cu — bn_mul_ntt: exact FFT multiplication over word-size primes.
+//
+// The paper's §4: transform A and B over a prime field
+// Z_p with p = k 2^n + 1, multiply pointwise, transform
+// back, then resolve the carries by a scan-add (bmulFFT, Fig. 9,
+// PAPER.md:767-788, splitFftReg/publish PAPER.md:816-821).  The printed
+// digit scheme is inexact (readings R10/R11), so this kernel uses
+// the exact variant: the u32 limbs ARE the digits, both operands are
+// zero-padded to N = 2m points, and three primes p0 < p1 < p2 < 2^30 with
+// Garner CRT recover every coefficient c_k <= m (2^32-1)^2 < 2^77 < p0 p1 p2.
+//
+// One instance per TPI = N/16 threads (IPB instances per CTA); each thread
+// holds R = 16 elements in registers and performs 4 radix-2 stages per
+// register pass; passes exchange through a shared buffer X with an XOR
+// swizzle that makes every pass's access pattern bank-conflict free.
+//   forward  : DIF (Gentleman–Sande), natural in -> bit-reversed out,
+//              Harvey-lazy values in [0, 2p), Shoup twiddle products;
+//   pointwise: Montgomery product (R = 2^32), values stay in [0, 2p);
+//   inverse  : DIT (Cooley–Tukey) with omega^-1, bit-reversed in -> natural
+//              out, values in [0, 4p); 1/N and R are folded into the CRT
+//              constants (PAPER.md:764's "scale by invM" moved into Garner).
+// Because the DIF output order is exactly the DIT input order, no bit
+// reversal is ever performed, and the last forward pass / pointwise product
+// / first inverse pass happen in registers without a shared-memory trip.
+// Per thread, then, 8 consecutive coefficients are CRT'd and aggregated into
+// 8 low words + 2 overflow words (< 2^46), published into L/H exactly like
+// the classical kernel (reading R8) and resolved by the §2 scan-add.
+#include "bn_common.cuh"
+#include "bn_kernels.h"
+
+namespace bn {
+
+__constant__ PrimeConst c_pc[kNumPrimes];
+__constant__ CrtConst c_crt[kMaxLogN + 1];
+
+cudaError_t upload_prime_consts(const PrimeConst (&pc)[kNumPrimes], const CrtConst (&crt)[kMaxLogN + 1]) {
+  cudaError_t e = cudaMemcpyToSymbol(c_pc, pc, sizeof(pc));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_crt, crt, sizeof(crt));
+}
+
+// ------------------------------------------------------------ field arithmetic
+// Shoup: w < p, wsh = floor(w 2^32 / p); any x < 2^32 -> x w mod p in [0, 2p).
+BN_DEV uint32_t shoup(uint32_t x, uint32_t w, uint32_t wsh, uint32_t p) {
+  const uint32_t q = __umulhi(x, wsh);
+  return x * w - q * p;
+}
+// x < 2m -> x mod m (one VIADDMNMX: min(x, x - m) as unsigned)
+BN_DEV uint32_t red2(uint32_t x, uint32_t m) { return min(x, x - m); }
+// Montgomery: a, b < 2p, p < 2^30 -> a b 2^-32 mod p in [0, 2p)
+BN_DEV uint32_t mont(uint32_t a, uint32_t b, uint32_t p, uint32_t pinv) {
+  const uint64_t t = (uint64_t)a * b;
+  const uint32_t m = (uint32_t)t * pinv;
+  const uint64_t u = t + (uint64_t)m * p;
+  return (uint32_t)(u >> 32);
+}
+// DIF butterfly, inputs [0, 2p) -> outputs [0, 2p)
+BN_DEV void gs_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p, uint32_t p2) {
+  const uint32_t s = x + y;
+  const uint32_t d = x - y + p2;
+  x = red2(s, p2);
+  y = shoup(d, w.x, w.y, p);
+}
+// DIT butterfly, inputs [0, 4p) -> outputs [0, 4p)
+BN_DEV void ct_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p, uint32_t p2) {
+  const uint32_t u = red2(x, p2);
+  const uint32_t v = shoup(y, w.x, w.y, p);
+  x = u + v;
+  y = u - v + p2;
+}
+
+// ------------------------------------------------------------ layout
+template <int LOGN>
+struct NttCfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int M = N / 2;
+  static constexpr int R = 16;
+  static constexpr int TPI = N / R;
+  static constexpr int NP = (LOGN + 3) / 4;  // register passes
+  static constexpr int IPB = TPI >= 256 ? 1 : 256 / TPI;
+  static constexpr int T = IPB * TPI;
+  static constexpr int SMEM_WORDS = IPB * (N + 3 * M) + T / 32;
+};
+
+// pass P covers forward stages [S0, S1); its 16 register elements are the
+// indices whose bits [LO, LO+4) vary (all other bits come from the thread id).
+template <int LOGN, int P>
+struct PassCfg {
+  static constexpr int S0 = 4 * P;
+  static constexpr int S1 = (4 * P + 4 < LOGN) ? 4 * P + 4 : LOGN;
+  static constexpr int LO = (LOGN - 4 * (P + 1)) > 0 ? LOGN - 4 * (P + 1) : 0;
+};
+
+template <int LO>
+BN_DEV int lay(int t, int e) {
+  return (t & ((1 << LO) - 1)) | (e << LO) | ((t >> LO) << (LO + 4));
+}
+// Bank swizzle: XOR row bits r and r<<1 into the column (conflict
+// free for every pass pattern, proven in tests/test_ntt_layout.py).
+BN_DEV int swz(int u) {
+  const int r = (u >> 5) & 15;
+  return u ^ (r ^ (r << 1));
+}
+
+template <int TPI>
+BN_DEV void bar() {
+  if constexpr (TPI <= 32) __syncwarp();
+  else __syncthreads();
+}
+
+template <int LOGN, int P, bool PADDED>
+BN_DEV void fwd_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
+  using PS = PassCfg<LOGN, P>;
+  const int tlow = t & ((1 << PS::LO) - 1);
+#pragma unroll
+  for (int s = PS::S0; s < PS::S1; s++) {
+    const int b = (LOGN - 1 - s) - PS::LO;
+    const uint2* Ts = tw + ((1 << LOGN) - ((1 << LOGN) >> s)) + tlow;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      if (e & (1 << b)) continue;
+      const int el = e & ((1 << b) - 1);
+      const uint2 w = __ldg(Ts + (el << PS::LO));
+      if (PADDED && P == 0 && s == 0) {
+        // zero-padded input: x[e | 8] == 0, so (x + 0, (x - 0) w)
+        x[e | (1 << b)] = shoup(x[e], w.x, w.y, p);
+      } else {
+        gs_bfly(x[e], x[e | (1 << b)], w, p, p2);
+      }
+    }
+  }
+}
+
+template <int LOGN, int P>
+BN_DEV void inv_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
+  using PS = PassCfg<LOGN, P>;
+  const int tlow = t & ((1 << PS::LO) - 1);
+#pragma unroll
+  for (int s = PS::S1 - 1; s >= PS::S0; s--) {
+    const int b = (LOGN - 1 - s) - PS::LO;
+    const uint2* Ts = tw + ((1 << LOGN) - ((1 << LOGN) >> s)) + tlow;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      if (e & (1 << b)) continue;
+      const int el = e & ((1 << b) - 1);
+      const uint2 w = __ldg(Ts + (el << PS::LO));
+      ct_bfly(x[e], x[e | (1 << b)], w, p, p2);
+    }
+  }
+}
+
+template <int LO_FROM, int LO_TO, int TPI>
+BN_DEV void xchg(uint32_t (&x)[16], uint32_t* X, int t) {
+  bar<TPI>();  // previous readers of X are done
+#pragma unroll
+  for (int e = 0; e < 16; e++) X[swz(lay<LO_FROM>(t, e))] = x[e];
+  bar<TPI>();
+#pragma unroll
+  for (int e = 0; e < 16; e++) x[e] = X[swz(lay<LO_TO>(t, e))];
+}
+
+template <int LOGN, bool PADDED>
+BN_DEV void fwd_all(uint32_t (&x)[16], uint32_t* X, int t, const uint2* tw, uint32_t p, uint32_t p2) {
+  using C = NttCfg<LOGN>;
+  fwd_pass<LOGN, 0, PADDED>(x, t, tw, p, p2);
+  if constexpr (C::NP > 1) {
+    xchg<PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X, t);
+    fwd_pass<LOGN, 1, PADDED>(x, t, tw, p, p2);
+  }
+  if constexpr (C::NP > 2) {
+    xchg<PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X, t);
+    fwd_pass<LOGN, 2, PADDED>(x, t, tw, p, p2);
+  }
+  if constexpr (C::NP > 3) {
+    xchg<PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, C::TPI>(x, X, t);
+    fwd_pass<LOGN, 3, PADDED>(x, t, tw, p, p2);
+  }
+  static_assert(C::NP <= 4, "LOGN <= 16");
+}
+
+template <int LOGN>
+BN_DEV void inv_all(uint32_t (&x)[16], uint32_t* X, int t, const uint2* tw, uint32_t p, uint32_t p2) {
+  using C = NttCfg<LOGN>;
+  if constexpr (C::NP > 3) {
+    inv_pass<LOGN, 3>(x, t, tw, p, p2);
+    xchg<PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X, t);
+  }
+  if constexpr (C::NP > 2) {
+    inv_pass<LOGN, 2>(x, t, tw, p, p2);
+    xchg<PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X, t);
+  }
+  if constexpr (C::NP > 1) {
+    inv_pass<LOGN, 1>(x, t, tw, p, p2);
+    xchg<PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, C::TPI>(x, X, t);
+  }
+  inv_pass<LOGN, 0>(x, t, tw, p, p2);
+}
+
+// 3-word accumulate (a0, a1, a2) += (c0, c1, c2)
+BN_DEV void add3(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t c0, uint32_t c1, uint32_t c2) {
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+      : "+r"(a0), "+r"(a1), "+r"(a2)
+      : "r"(c0), "r"(c1), "r"(c2));
+}
+
+// ------------------------------------------------------------ the kernel
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+    mul_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                   const uint2* __restrict__ tw) {
+  using C = NttCfg<LOGN>;
+  constexpr int N = C::N, M = C::M, TPI = C::TPI;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int slot = threadIdx.x / TPI;
+  const int t = threadIdx.x % TPI;
+  uint32_t* X = sm + slot * N;                       // exchange buffer, later L | H
+  uint32_t* Res = sm + C::IPB * N + slot * (3 * M);  // raw inverse outputs per prime
+  uint32_t* agg = sm + C::IPB * (N + 3 * M);
+
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t inst = grp * C::IPB + slot;
+    const bool valid = inst < n_inst;
+    const uint32_t* ai = a + (valid ? inst : 0) * M;
+    const uint32_t* bi = b + (valid ? inst : 0) * M;
+
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv, one_sh = c_pc[j].one_sh;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t x[16], ah[16];
+#pragma unroll 1
+      for (int op = 0; op < 2; op++) {
+        // N-1: reduce the limbs mod p into pass-0 layout (index t + e N/16),
+        // upper half is the zero padding (reading R11)
+        const uint32_t* src = op == 0 ? ai : bi;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          const uint32_t v = valid ? __ldg(src + t + e * (N / 16)) : 0u;
+          x[e] = v - __umulhi(v, one_sh) * p;  // Shoup by 1 -> [0, 2p)
+        }
+#pragma unroll
+        for (int e = 8; e < 16; e++) x[e] = 0u;
+        // N-2: forward transform
+        fwd_all<LOGN, true>(x, X, t, twf, p, p2);
+        if (op == 0) {
+#pragma unroll
+          for (int e = 0; e < 16; e++) ah[e] = x[e];
+        }
+      }
+      // N-3: pointwise product (same register layout for A-hat and B-hat)
+#pragma unroll
+      for (int e = 0; e < 16; e++) x[e] = mont(ah[e], x[e], p, pinv);
+      // N-4: inverse transform -> pass-0 layout, natural order
+      inv_all<LOGN>(x, X, t, twi, p, p2);
+      // keep coefficients 0..M-1 (truncated product): e < 8
+#pragma unroll
+      for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
+    }
+    bar<TPI>();
+
+    // N-5 / N-6: Garner CRT of 8 consecutive coefficients, aggregate, publish
+    {
+      const CrtConst& k = c_crt[LOGN];
+      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+      uint32_t y0[8], y1[8], y2[8];
+      lds_limbs<8>(y0, Res + 0 * M + 8 * t);
+      lds_limbs<8>(y1, Res + 1 * M + 8 * t);
+      lds_limbs<8>(y2, Res + 2 * M + 8 * t);
+      uint32_t lows[8], hs[8];
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+        const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+        const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+        const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+        const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+        const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+        const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+        const uint32_t d = red2(b2v + c2v, 2 * p2);
+        const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+        // c = r0 + p0 t1 + p0 p1 t2  (< 2^90)
+        const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+        const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+        const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
+        add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
+        lows[q] = a0;
+        a0 = a1;
+        a1 = a2;
+        a2 = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      // X is dead (last exchange read it before inv_pass<0>, followed by bar)
+      uint32_t* L = X;
+      uint32_t* H = X + M;
+      sts_limbs<8>(L + 8 * t, lows);
+      if (8 * t + 8 < M) {
+        sts_limbs<8>(H + 8 * t + 8, hs);
+      } else {
+        uint32_t z[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) z[q] = 0;
+        sts_limbs<8>(H, z);
+      }
+    }
+    bar<TPI>();
+    // N-7: R = L + H, store
+    {
+      uint32_t xl[8], yh[8], r[8];
+      lds_limbs<8>(xl, X + 8 * t);
+      lds_limbs<8>(yh, X + M + 8 * t);
+      add_regs<8, TPI>(xl, yh, r, valid, agg);
+      if (valid) store_limbs<8>(out + inst * M + 8 * t, r);
+    }
+    __syncthreads();  // X / Res / agg reused by the next group
+  }
+}
+
+// Forward transform only (tests): rows of N residues < p, in place,
+// bit-reversed output in [0, p).
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+    ntt_forward_debug_kernel(uint32_t* xg, uint64_t n_inst, const uint2* __restrict__ tw, int j) {
+  using C = NttCfg<LOGN>;
+  constexpr int N = C::N;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int slot = threadIdx.x / C::TPI;
+  const int t = threadIdx.x % C::TPI;
+  uint32_t* X = sm + slot * N;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t inst = grp * C::IPB + slot;
+    const bool valid = inst < n_inst;
+    uint32_t* row = xg + (valid ? inst : 0) * N;
+    const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2;
+    uint32_t x[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) x[e] = valid ? row[t + e * (N / 16)] : 0u;
+    fwd_all<LOGN, false>(x, X, t, tw + 2 * j * (N - 1), p, p2);
+    constexpr int LO_LAST = PassCfg<LOGN, C::NP - 1>::LO;
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < 16; e++) row[lay<LO_LAST>(t, e)] = red2(x[e], p);
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                const NttTables& tb, cudaStream_t st, int n_sm) {
+  using C = NttCfg<LOGN>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(mul_ntt_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_ntt_kernel<LOGN>, C::T, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
+  const unsigned grid = (unsigned)(n_groups < cap ? n_groups : cap);
+  mul_ntt_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw);
+  return cudaGetLastError();
+}
+
+template <int LOGN>
+static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const NttTables& tb,
+                                cudaStream_t st) {
+  using C = NttCfg<LOGN>;
+  constexpr size_t smem = (size_t)C::IPB * C::N * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(ntt_forward_debug_kernel<LOGN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  const unsigned grid = (unsigned)(n_groups < 65535 ? n_groups : 65535);
+  ntt_forward_debug_kernel<LOGN><<<grid, C::T, smem, st>>>(x, n_inst, tb.tw, prime);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                           uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm) {
+  switch (logm + 1) {
+    case 6: return launch_ntt_t<6>(out, a, b, n_inst, tb, st, n_sm);
+    case 7: return launch_ntt_t<7>(out, a, b, n_inst, tb, st, n_sm);
+    case 8: return launch_ntt_t<8>(out, a, b, n_inst, tb, st, n_sm);
+    case 9: return launch_ntt_t<9>(out, a, b, n_inst, tb, st, n_sm);
+    case 10: return launch_ntt_t<10>(out, a, b, n_inst, tb, st, n_sm);
+    case 11: return launch_ntt_t<11>(out, a, b, n_inst, tb, st, n_sm);
+    case 12: return launch_ntt_t<12>(out, a, b, n_inst, tb, st, n_sm);
+    case 13: return launch_ntt_t<13>(out, a, b, n_inst, tb, st, n_sm);
+    case 14: return launch_ntt_t<14>(out, a, b, n_inst, tb, st, n_sm);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_ntt_forward_debug(int lgn, uint32_t* x, uint64_t n_inst, int prime, const NttTables& tb,
+                                     cudaStream_t st) {
+  switch (lgn) {
+    case 6: return launch_dbg_t<6>(x, n_inst, prime, tb, st);
+    case 7: return launch_dbg_t<7>(x, n_inst, prime, tb, st);
+    case 8: return launch_dbg_t<8>(x, n_inst, prime, tb, st);
+    case 9: return launch_dbg_t<9>(x, n_inst, prime, tb, st);
+    case 10: return launch_dbg_t<10>(x, n_inst, prime, tb, st);
+    case 11: return launch_dbg_t<11>(x, n_inst, prime, tb, st);
+    case 12: return launch_dbg_t<12>(x, n_inst, prime, tb, st);
+    case 13: return launch_dbg_t<13>(x, n_inst, prime, tb, st);
+    case 14: return launch_dbg_t<14>(x, n_inst, prime, tb, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace bn

@@ -1,0 +1,98 @@
+"""CPU model of the NTT kernel's data layout (mul_ntt.cu) — -m "not gpu".
+
+Checks the index algebra the kernel relies on, for every N = 2^6 .. 2^14:
+* pass p's 16 register elements of thread t are indices whose bits
+  [LO_p, LO_p + 4) vary, and every forward stage s of the pass pairs elements
+  held by the same thread (butterfly partner u ^ 2^(N-1-s));
+* the per-stage twiddle index (u mod 2^beta) is tlow + (e_low << LO);
+* the XOR swizzle swz(u) = u ^ (r ^ (r << 1)), r = (u >> 5) & 15, is a
+  bijection on [0, N) and every warp access of every pass is
+  bank-conflict-free (32 distinct banks per 4-byte access);
+* the L/H publish of the CRT epilogue (Q = 8 consecutive coefficients per
+  thread) never writes one H slot twice and covers every slot.
+"""
+import pytest
+
+R_LOG = 4
+
+
+def passes(logn):
+    np_ = (logn + 3) // 4
+    out = []
+    for p in range(np_):
+        s0 = 4 * p
+        s1 = min(4 * p + 4, logn)
+        lo = max(logn - 4 * (p + 1), 0)
+        out.append((s0, s1, lo))
+    return out
+
+
+def lay(t, e, lo):
+    return (t & ((1 << lo) - 1)) | (e << lo) | ((t >> lo) << (lo + 4))
+
+
+def swz(u):
+    r = (u >> 5) & 15
+    return u ^ (r ^ (r << 1))
+
+
+@pytest.mark.parametrize("logn", range(6, 15))
+def test_pass_groups_and_twiddle_index(logn):
+    N = 1 << logn
+    tpi = N >> R_LOG
+    for (s0, s1, lo) in passes(logn):
+        seen = set()
+        for t in range(tpi):
+            us = [lay(t, e, lo) for e in range(16)]
+            seen.update(us)
+            for s in range(s0, s1):
+                beta = logn - 1 - s
+                b = beta - lo
+                assert 0 <= b < 4
+                for e in range(16):
+                    if e & (1 << b):
+                        continue
+                    u, v = us[e], us[e | (1 << b)]
+                    assert v == u + (1 << beta)                  # DIF partner
+                    j = u & ((1 << beta) - 1)                     # twiddle exponent / 2^s
+                    tlow = t & ((1 << lo) - 1)
+                    assert j == tlow + ((e & ((1 << b) - 1)) << lo)
+        assert seen == set(range(N))                              # a partition of [0, N)
+
+
+@pytest.mark.parametrize("logn", range(6, 15))
+def test_swizzle_bijective_and_conflict_free(logn):
+    N = 1 << logn
+    tpi = N >> R_LOG
+    assert sorted(swz(u) for u in range(N)) == list(range(N))
+    for (_, _, lo) in passes(logn):
+        for w0 in range(0, max(tpi, 32), 32):
+            lanes = [t for t in range(w0, w0 + 32)]
+            for e in range(16):
+                if tpi >= 32:
+                    banks = {swz(lay(t, e, lo)) % 32 for t in lanes}
+                    assert len(banks) == 32, (logn, lo, e)
+                else:
+                    # several instances per warp: each instance has its own N-word buffer
+                    addrs = {(t // tpi) * N + swz(lay(t % tpi, e, lo)) for t in lanes}
+                    banks = {a % 32 for a in addrs}
+                    # distinct instances' buffers start at multiples of N (>= 64 words):
+                    # conflicts are at most the number of instances sharing a bank
+                    assert len(addrs) == 32
+                    assert max(sum(1 for a in addrs if a % 32 == bk) for bk in banks) <= 32 // tpi
+
+
+@pytest.mark.parametrize("logn", range(6, 15))
+def test_epilogue_publish_layout(logn):
+    M = 1 << (logn - 1)
+    tpi = (1 << logn) >> R_LOG
+    Q = M // tpi
+    assert Q == 8
+    writes = {}
+    for t in range(tpi):
+        for q in range(Q):
+            base = Q * t + Q if Q * t + Q < M else 0
+            slot = base + q
+            assert slot not in writes
+            writes[slot] = t
+    assert set(writes) == set(range(M))
