@@ -98,13 +98,17 @@ BN_DEV void chunk_sum(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (
   }
 }
 
-// Step (3): ripple the chunk's carry-in through its limbs.
+// Step (3): r_i = p_i + carry_i, where carry_i is the
+// exclusive scan value at limb i: the chunk's carry-in rippled through the
+// thread's own limbs together with their generates (ov) and propagates (mx).
 template <int L>
-BN_DEV void chunk_apply(uint32_t (&s)[L], uint32_t cin) {
+BN_DEV void chunk_apply(const uint32_t (&x)[L], uint32_t (&s)[L], uint32_t cin) {
 #pragma unroll
   for (int i = 0; i < L; i++) {
-    uint32_t r = s[i] + cin;
-    cin = cin & (s[i] == 0xFFFFFFFFu);
+    const uint32_t ov = s[i] < x[i];
+    const uint32_t mx = s[i] == 0xFFFFFFFFu;
+    const uint32_t r = s[i] + cin;
+    cin = ov | (mx & cin);
     s[i] = r;
   }
 }
@@ -160,7 +164,7 @@ BN_DEV void add_regs(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&
   chunk_sum<L>(x, y, r, g, p);
   if (!valid) g = p = 0;
   uint32_t cin = carry_scan<TPI>(g, p, agg);
-  chunk_apply<L>(r, cin);
+  chunk_apply<L>(x, r, cin);
 }
 
 }  // namespace bn

@@ -129,3 +129,51 @@ def test_literal_segmented_scan_leaks():
         flags.append((4 if i % M == 0 else 0) | ((p == MAX) << 1) | int(p < x))
     carries = _excl_scan(carry_op_sgm, 2, flags)
     assert carries[2] & 1 == 1  # the carry of instance 0 leaks into instance 1
+
+
+def _model_add(xs, ys, L, TPI):
+    """Python model of csrc/bn_common.cuh add_regs over one instance:
+    chunk_sum -> ballot-add carry scan across TPI threads -> chunk_apply."""
+    MAX = 0xFFFFFFFF
+    gs, ps, sums = [], [], []
+    for t in range(TPI):
+        x, y = xs[t * L:(t + 1) * L], ys[t * L:(t + 1) * L]
+        s = [(a + b) & MAX for a, b in zip(x, y)]
+        g, p = 0, 1
+        for a, v in zip(x, s):
+            ov, mx = int(v < a), int(v == MAX)
+            g = ov | (mx & g)
+            p &= mx
+        gs.append(g)
+        ps.append(p)
+        sums.append(s)
+    cins, _ = _ballot_cin(gs, ps, 0, TPI)
+    out = []
+    for t in range(TPI):
+        x, s, c = xs[t * L:(t + 1) * L], sums[t], cins[t]
+        for a, v in zip(x, s):
+            out.append((v + c) & MAX)
+            c = int(v < a) | (int(v == MAX) & c)
+    return out
+
+
+def test_model_add_matches_python_int():
+    rng = random.Random(11)
+    for L, TPI in ((8, 4), (8, 32), (4, 16), (16, 8)):
+        M = L * TPI
+        for trial in range(300):
+            kind = trial % 4
+            if kind == 0:
+                xs = [rng.getrandbits(32) for _ in range(M)]
+                ys = [rng.getrandbits(32) for _ in range(M)]
+            elif kind == 1:
+                xs, ys = [0xFFFFFFFF] * M, [1] + [0] * (M - 1)
+            elif kind == 2:
+                xs = [rng.getrandbits(32) for _ in range(M)]
+                ys = [(~v + (rng.random() < 0.05)) & 0xFFFFFFFF for v in xs]
+            else:
+                xs, ys = [0xFFFFFFFF] * M, [0xFFFFFFFF] * M
+            A = sum(v << (32 * i) for i, v in enumerate(xs))
+            B = sum(v << (32 * i) for i, v in enumerate(ys))
+            S = (A + B) % (1 << (32 * M))
+            assert _model_add(xs, ys, L, TPI) == [(S >> (32 * i)) & 0xFFFFFFFF for i in range(M)]
