@@ -70,6 +70,19 @@ BN_DEV void sts_limbs(uint32_t* dst, const uint32_t (&r)[L]) {
     reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
 }
 
+// cp.async (LDGSTS) 16-byte global -> shared copy; !valid zero-fills the
+// destination without reading the source.
+BN_DEV void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc), "r"(sz) : "memory");
+}
+BN_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+BN_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------- carry scan
 
 // Mask with bit l set for every lane l that is the top lane of a TPI-lane

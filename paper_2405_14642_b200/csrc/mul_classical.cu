@@ -53,38 +53,58 @@ struct MulCCfg {
   // 128-bit window loads of the 8 lanes (inst_lo, g) of a quarter-warp conflict-free
   static constexpr int BS = I >= 8 ? 1 : 8 / I;
   static constexpr int SB = M + Q + (((4 * BS - Q) % 32) + 32) % 32;
-  static constexpr int SMEM_WORDS = IPB * (SA + SB) + T / 32;
+  static constexpr int STAGE_WORDS = IPB * (SA + SB);      // one group's A and B
+  static constexpr int SMEM_WORDS = 2 * STAGE_WORDS + T / 32;  // double-buffered
   static constexpr int MINB = T >= 1024 ? 1 : 2048 / T / 2;    // target residency
   static_assert(Q >= 2 && (Q % 4) == 0, "Q must be a multiple of 4 (>= 2 for the L/H layout)");
   static_assert(G >= 1, "size too small for Q");
 };
 
+// One Q x Q block of partial products: column q gets A[i] * B[j] for the Q
+// consecutive i of `av` and the window B[k1 + q - i] held in cur / prev.
+template <int Q>
+BN_DEV void mac_block(uint32_t (&lo)[Q], uint32_t (&hi)[Q], uint32_t (&top)[Q], const uint32_t (&av)[Q],
+                      const uint32_t (&cur)[Q], const uint32_t (&prev)[Q]) {
+#pragma unroll
+  for (int s = 0; s < Q; s++) {
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int d = q - s;
+      mac3(lo[q], hi[q], top[q], av[s], d >= 0 ? cur[d] : prev[Q + d]);
+    }
+  }
+}
+
 // Q column sums starting at column Q*j0 (Fig. 7 convolution + combine).
 // Ash: instance A (A[i] at Ash[i]); Bsh: instance B with B[x] at Bsh[x],
-// B[-Q..-1] == 0.
+// B[-Q..-1] == 0.  Block c covers i in [Q c, Q c + Q) against B chunks
+// j0 - c (cur) and j0 - c - 1 (prev); two blocks per trip so the window
+// registers swap roles instead of being copied.
 template <int Q>
 BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_t (&lhcs)[Q + 2]) {
   uint32_t lo[Q], hi[Q], top[Q];
 #pragma unroll
   for (int q = 0; q < Q; q++) lo[q] = hi[q] = top[q] = 0;
-  uint32_t cur[Q], prev[Q];
-  lds_limbs<Q>(cur, Bsh + Q * j0);
+  uint32_t b0[Q], b1[Q], av[Q];
+  lds_limbs<Q>(b0, Bsh + Q * j0);
+  const uint32_t* ap = Ash;
+  const uint32_t* bp = Bsh + Q * (j0 - 1);
+  int c = j0 + 1;  // blocks left
 #pragma unroll 1
-  for (int c = 0; c <= j0; c++) {
-    uint32_t av[Q];
-    lds_limbs<Q>(av, Ash + Q * c);
-    lds_limbs<Q>(prev, Bsh + Q * (j0 - c - 1));
-#pragma unroll
-    for (int s = 0; s < Q; s++) {
-#pragma unroll
-      for (int q = 0; q < Q; q++) {
-        const int d = q - s;
-        const uint32_t bj = d >= 0 ? cur[d] : prev[Q + d];
-        mac3(lo[q], hi[q], top[q], av[s], bj);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < Q; q++) cur[q] = prev[q];
+  for (; c >= 2; c -= 2) {
+    lds_limbs<Q>(av, ap);
+    lds_limbs<Q>(b1, bp);
+    mac_block<Q>(lo, hi, top, av, b0, b1);
+    lds_limbs<Q>(av, ap + Q);
+    lds_limbs<Q>(b0, bp - Q);
+    mac_block<Q>(lo, hi, top, av, b1, b0);
+    ap += 2 * Q;
+    bp -= 2 * Q;
+  }
+  if (c) {
+    lds_limbs<Q>(av, ap);
+    lds_limbs<Q>(b1, bp);
+    mac_block<Q>(lo, hi, top, av, b0, b1);
   }
   // combine: accum = (lo, hi), carry = top
   lhcs[0] = lo[0];
@@ -106,9 +126,7 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
   using C = MulCCfg<LOGM, Q>;
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* As = sm;                    // IPB * SA
-  uint32_t* Bs = sm + C::IPB * C::SA;   // IPB * SB  (B[x] at Bs[k*SB + Q + x])
-  uint32_t* agg = Bs + C::IPB * C::SB;  // T/32
+  uint32_t* agg = sm + 2 * C::STAGE_WORDS;  // T/32
 
   const int t = threadIdx.x;
   // convolution mapping: lane = inst_lo + I * g_lo (instance-fastest)
@@ -120,24 +138,40 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
   const int add_slot = t / C::G;
   const int chunk = t % C::G;
 
-  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-    const uint64_t inst0 = grp * C::IPB;
-    // ---- stage A, B: coalesced 128-bit loads -> shared
-    constexpr int VPI = M / 4;  // uint4 per instance operand
+  // B[-Q..-1] = 0 in both stages (never overwritten: loads and H start at B[0])
+  for (int v = t; v < 2 * C::IPB * Q; v += C::T) {
+    const int st = v / (C::IPB * Q), k = (v / Q) % C::IPB;
+    sm[st * C::STAGE_WORDS + C::IPB * C::SA + k * C::SB + (v % Q)] = 0u;
+  }
+  // stage A, B of a group with cp.async: coalesced 16-byte
+  // copies global -> shared, zero-filled past the last instance
+  constexpr int VPI = M / 4;  // uint4 per instance operand
+  auto issue = [&](uint64_t grp, int st) {
+    uint32_t* As = sm + st * C::STAGE_WORDS;
+    uint32_t* Bs = As + C::IPB * C::SA;
+    const uint64_t i0 = grp * C::IPB;
     for (int v = t; v < C::IPB * VPI; v += C::T) {
       const int k = v / VPI, w = (v % VPI) * 4;
-      const uint64_t inst = inst0 + k;
-      uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
-      if (inst < n_inst) {
-        x = ldg_stream(reinterpret_cast<const uint4*>(a + inst * M + w));
-        y = ldg_stream(reinterpret_cast<const uint4*>(b + inst * M + w));
-      }
-      *reinterpret_cast<uint4*>(As + k * C::SA + w) = x;
-      *reinterpret_cast<uint4*>(Bs + k * C::SB + Q + w) = y;
+      const bool ok = i0 + k < n_inst;
+      const uint64_t off = ok ? (i0 + k) * M + w : 0;
+      cp_async16(As + k * C::SA + w, a + off, ok);
+      cp_async16(Bs + k * C::SB + Q + w, b + off, ok);
     }
-    for (int v = t; v < C::IPB * Q; v += C::T) Bs[(v / Q) * C::SB + (v % Q)] = 0u;  // B[-Q..-1]
+  };
+
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  uint64_t grp = blockIdx.x;
+  if (grp < n_groups) issue(grp, 0);
+  cp_async_commit();
+  for (int st = 0; grp < n_groups; grp += gridDim.x, st ^= 1) {
+    // prefetch the next group into the other stage while this one computes
+    if (grp + gridDim.x < n_groups) issue(grp + gridDim.x, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    uint32_t* As = sm + st * C::STAGE_WORDS;
+    uint32_t* Bs = As + C::IPB * C::SA;
+    const uint64_t inst0 = grp * C::IPB;
 
     // ---- convolution: low chunk j0 = g and mirror chunk j0' = M/Q - 1 - g
     uint32_t lh0[Q + 2], lh1[Q + 2];
@@ -189,8 +223,9 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
       add_regs<L2, C::G>(x, y, res, valid, agg);
       if (valid) store_limbs<L2>(out + inst * M + L2 * chunk, res);
     }
-    __syncthreads();  // smem reused by the next group
+    __syncthreads();  // this stage is refilled two groups from now
   }
+  cp_async_wait<0>();
 }
 
 template <int LOGM>
@@ -203,7 +238,11 @@ static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  const uint64_t cap = (uint64_t)n_sm * C::MINB * 16;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_classical_kernel<LOGM, Q>, C::T, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;  // persistent: one wave of resident CTAs
   const unsigned grid = (unsigned)(n_groups < cap ? n_groups : cap);
   mul_classical_kernel<LOGM, Q><<<grid, C::T, smem, st>>>(out, a, b, n_inst);
   return cudaGetLastError();

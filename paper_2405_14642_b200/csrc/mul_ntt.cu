@@ -79,7 +79,11 @@ struct NttCfg {
   static constexpr int NP = (LOGN + 3) / 4;  // register passes
   static constexpr int IPB = TPI >= 256 ? 1 : 256 / TPI;
   static constexpr int T = IPB * TPI;
-  static constexpr int SMEM_WORDS = IPB * (N + 3 * M) + T / 32;
+  // exchange area (padded by 1/16 for LOGN <= 8, see xbase), raw residues, agg
+  static constexpr int XW = LOGN <= 8 ? IPB * N + (IPB * N >> 4) : IPB * N;
+  static constexpr int SMEM_WORDS = XW + IPB * 3 * M + T / 32;
+  // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
+  static constexpr int MINB = T <= 256 ? (LOGN <= 8 ? 4 : 3) : 1;
 };
 
 // pass P covers forward stages [S0, S1); its 16 register elements are the
@@ -120,6 +124,14 @@ BN_DEV void fwd_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uin
     for (int e = 0; e < 16; e++) {
       if (e & (1 << b)) continue;
       const int el = e & ((1 << b) - 1);
+      if (PS::LO == 0 && el == 0) {
+        // twiddle w^0 = 1 (exponent j = tlow + el << LO = 0 for every thread):
+        // no multiplication, only the lazy reductions
+        const uint32_t xs = x[e], ys = x[e | (1 << b)];
+        x[e] = red2(xs + ys, p2);
+        x[e | (1 << b)] = red2(xs - ys + p2, p2);
+        continue;
+      }
       const uint2 w = __ldg(Ts + (el << PS::LO));
       if (PADDED && P == 0 && s == 0) {
         // zero-padded input: x[e | 8] == 0, so (x + 0, (x - 0) w)
@@ -143,55 +155,91 @@ BN_DEV void inv_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uin
     for (int e = 0; e < 16; e++) {
       if (e & (1 << b)) continue;
       const int el = e & ((1 << b) - 1);
+      if (PS::LO == 0 && el == 0) {  // w^0 = 1
+        const uint32_t u = red2(x[e], p2), v = red2(x[e | (1 << b)], p2);
+        x[e] = u + v;
+        x[e | (1 << b)] = u - v + p2;
+        continue;
+      }
       const uint2 w = __ldg(Ts + (el << PS::LO));
       ct_bfly(x[e], x[e | (1 << b)], w, p, p2);
     }
   }
 }
 
-template <int LO_FROM, int LO_TO, int TPI>
-BN_DEV void xchg(uint32_t (&x)[16], uint32_t* X, int t) {
+// Exchange-buffer addressing.  X0 = the CTA's exchange area, xo = slot * N;
+// element (t, e) of a pass with low bit LO lives at CTA-wide index
+// u = xo + T(t) + (e << LO), T(t) = the thread's bits outside [LO, LO+4).
+//  * LOGN <= 8 (several instances per warp): additive pad u + (u >> 4) —
+//    bank-conflict free for every pass pattern of these sizes
+//    (tests/test_ntt_layout.py) and, being additive over the disjoint bit
+//    fields of T and e, the e part folds into the LDS/STS immediate offset.
+//  * LOGN >= 9: XOR swizzle swz (linear over XOR), split as
+//    swz(T) ^ [e part]: the e bits above bit 4 are added (disjoint bits),
+//    only the bank bits need one LOP3 per distinct constant.
+template <int LOGN, int LO>
+BN_DEV int xbase(int xo, int t) {
+  const int T = xo + ((t & ((1 << LO) - 1)) | ((t >> LO) << (LO + 4)));
+  if constexpr (LOGN <= 8) return T + (T >> 4);
+  else return swz(T);
+}
+template <int LOGN, int LO>
+BN_DEV int xaddr(int base, int e) {
+  const int E = e << LO;
+  if constexpr (LOGN <= 8) {
+    return base + E + (E >> 4);
+  } else {
+    const int hE = swz(E) ^ E;  // bank-bit part of the swizzle of E
+    if constexpr (LO >= 5) return (base ^ hE) + E;
+    else return (base ^ ((E & 31) ^ hE)) + (E & ~31);
+  }
+}
+
+template <int LOGN, int LO_FROM, int LO_TO, int TPI>
+BN_DEV void xchg(uint32_t (&x)[16], uint32_t* X0, int xo, int t) {
   bar<TPI>();  // previous readers of X are done
+  const int bw = xbase<LOGN, LO_FROM>(xo, t);
 #pragma unroll
-  for (int e = 0; e < 16; e++) X[swz(lay<LO_FROM>(t, e))] = x[e];
+  for (int e = 0; e < 16; e++) X0[xaddr<LOGN, LO_FROM>(bw, e)] = x[e];
   bar<TPI>();
+  const int br = xbase<LOGN, LO_TO>(xo, t);
 #pragma unroll
-  for (int e = 0; e < 16; e++) x[e] = X[swz(lay<LO_TO>(t, e))];
+  for (int e = 0; e < 16; e++) x[e] = X0[xaddr<LOGN, LO_TO>(br, e)];
 }
 
 template <int LOGN, bool PADDED>
-BN_DEV void fwd_all(uint32_t (&x)[16], uint32_t* X, int t, const uint2* tw, uint32_t p, uint32_t p2) {
+BN_DEV void fwd_all(uint32_t (&x)[16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p, uint32_t p2) {
   using C = NttCfg<LOGN>;
   fwd_pass<LOGN, 0, PADDED>(x, t, tw, p, p2);
   if constexpr (C::NP > 1) {
-    xchg<PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X, t);
+    xchg<LOGN, PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X0, xo, t);
     fwd_pass<LOGN, 1, PADDED>(x, t, tw, p, p2);
   }
   if constexpr (C::NP > 2) {
-    xchg<PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X, t);
+    xchg<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X0, xo, t);
     fwd_pass<LOGN, 2, PADDED>(x, t, tw, p, p2);
   }
   if constexpr (C::NP > 3) {
-    xchg<PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, C::TPI>(x, X, t);
+    xchg<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, C::TPI>(x, X0, xo, t);
     fwd_pass<LOGN, 3, PADDED>(x, t, tw, p, p2);
   }
   static_assert(C::NP <= 4, "LOGN <= 16");
 }
 
 template <int LOGN>
-BN_DEV void inv_all(uint32_t (&x)[16], uint32_t* X, int t, const uint2* tw, uint32_t p, uint32_t p2) {
+BN_DEV void inv_all(uint32_t (&x)[16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p, uint32_t p2) {
   using C = NttCfg<LOGN>;
   if constexpr (C::NP > 3) {
     inv_pass<LOGN, 3>(x, t, tw, p, p2);
-    xchg<PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X, t);
+    xchg<LOGN, PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X0, xo, t);
   }
   if constexpr (C::NP > 2) {
     inv_pass<LOGN, 2>(x, t, tw, p, p2);
-    xchg<PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X, t);
+    xchg<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X0, xo, t);
   }
   if constexpr (C::NP > 1) {
     inv_pass<LOGN, 1>(x, t, tw, p, p2);
-    xchg<PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, C::TPI>(x, X, t);
+    xchg<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, C::TPI>(x, X0, xo, t);
   }
   inv_pass<LOGN, 0>(x, t, tw, p, p2);
 }
@@ -205,7 +253,7 @@ BN_DEV void add3(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t c0, uint32_t
 
 // ------------------------------------------------------------ the kernel
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::T)
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
     mul_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                    const uint2* __restrict__ tw) {
   using C = NttCfg<LOGN>;
@@ -214,8 +262,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   const int slot = threadIdx.x / TPI;
   const int t = threadIdx.x % TPI;
   uint32_t* X = sm + slot * N;                       // exchange buffer, later L | H
-  uint32_t* Res = sm + C::IPB * N + slot * (3 * M);  // raw inverse outputs per prime
-  uint32_t* agg = sm + C::IPB * (N + 3 * M);
+  uint32_t* Res = sm + C::XW + slot * (3 * M);  // raw inverse outputs per prime
+  uint32_t* agg = sm + C::XW + C::IPB * (3 * M);
 
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
@@ -226,7 +274,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 
 #pragma unroll 1
     for (int j = 0; j < kNumPrimes; j++) {
-      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv, one_sh = c_pc[j].one_sh;
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
       const uint2* twf = tw + (2 * j + 0) * (N - 1);
       const uint2* twi = tw + (2 * j + 1) * (N - 1);
       uint32_t x[16], ah[16];
@@ -238,12 +286,13 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 #pragma unroll
         for (int e = 0; e < 8; e++) {
           const uint32_t v = valid ? __ldg(src + t + e * (N / 16)) : 0u;
-          x[e] = v - __umulhi(v, one_sh) * p;  // Shoup by 1 -> [0, 2p)
+          // a_i < 2^32 < 4p + 2p: two conditional subtractions of 2p -> [0, 2p)
+          x[e] = red2(red2(v, p2), p2);
         }
 #pragma unroll
         for (int e = 8; e < 16; e++) x[e] = 0u;
         // N-2: forward transform
-        fwd_all<LOGN, true>(x, X, t, twf, p, p2);
+        fwd_all<LOGN, true>(x, sm, slot * N, t, twf, p, p2);
         if (op == 0) {
 #pragma unroll
           for (int e = 0; e < 16; e++) ah[e] = x[e];
@@ -253,7 +302,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
 #pragma unroll
       for (int e = 0; e < 16; e++) x[e] = mont(ah[e], x[e], p, pinv);
       // N-4: inverse transform -> pass-0 layout, natural order
-      inv_all<LOGN>(x, X, t, twi, p, p2);
+      inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
       // keep coefficients 0..M-1 (truncated product): e < 8
 #pragma unroll
       for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
@@ -329,7 +378,6 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
   extern __shared__ __align__(16) uint32_t sm[];
   const int slot = threadIdx.x / C::TPI;
   const int t = threadIdx.x % C::TPI;
-  uint32_t* X = sm + slot * N;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
     const uint64_t inst = grp * C::IPB + slot;
@@ -339,7 +387,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
     uint32_t x[16];
 #pragma unroll
     for (int e = 0; e < 16; e++) x[e] = valid ? row[t + e * (N / 16)] : 0u;
-    fwd_all<LOGN, false>(x, X, t, tw + 2 * j * (N - 1), p, p2);
+    fwd_all<LOGN, false>(x, sm, slot * N, t, tw + 2 * j * (N - 1), p, p2);
     constexpr int LO_LAST = PassCfg<LOGN, C::NP - 1>::LO;
     if (valid) {
 #pragma unroll
@@ -372,7 +420,7 @@ template <int LOGN>
 static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const NttTables& tb,
                                 cudaStream_t st) {
   using C = NttCfg<LOGN>;
-  constexpr size_t smem = (size_t)C::IPB * C::N * sizeof(uint32_t);
+  constexpr size_t smem = (size_t)C::XW * sizeof(uint32_t);
   cudaError_t e = cudaFuncSetAttribute(ntt_forward_debug_kernel<LOGN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

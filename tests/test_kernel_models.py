@@ -168,11 +168,14 @@ def model_ntt_mul(A, B):
                             if e & (1 << b):
                                 continue
                             j = us[e] & ((1 << (logn - 1 - s)) - 1)
-                            wv = tw(w, s, j)
                             u_, v_ = x[e], x[e | (1 << b)]
                             assert u_ < p2 and v_ < p2
                             x[e] = red2((u_ + v_) & MASK, p2)
-                            x[e | (1 << b)] = shoup((u_ - v_ + p2) & MASK, wv, p)
+                            if lo == 0 and (e & ((1 << b) - 1)) == 0:   # w^0: no product
+                                assert j == 0
+                                x[e | (1 << b)] = red2((u_ - v_ + p2) & MASK, p2)
+                            else:
+                                x[e | (1 << b)] = shoup((u_ - v_ + p2) & MASK, tw(w, s, j), p)
                     for e in range(16):
                         X[us[e]] = x[e]
             return X
@@ -189,9 +192,12 @@ def model_ntt_mul(A, B):
                             if e & (1 << b):
                                 continue
                             j = us[e] & ((1 << (logn - 1 - s)) - 1)
-                            wv = tw(wi, s, j)
                             u_ = red2(x[e], p2)
-                            v_ = shoup(x[e | (1 << b)], wv, p)
+                            if lo == 0 and (e & ((1 << b) - 1)) == 0:   # w^0: no product
+                                assert j == 0
+                                v_ = red2(x[e | (1 << b)], p2)
+                            else:
+                                v_ = shoup(x[e | (1 << b)], tw(wi, s, j), p)
                             x[e] = (u_ + v_) & MASK
                             x[e | (1 << b)] = (u_ - v_ + p2) & MASK
                             assert x[e] < 4 * p and x[e | (1 << b)] < 4 * p
@@ -199,9 +205,9 @@ def model_ntt_mul(A, B):
                         X[us[e]] = x[e]
             return X
 
-        one_sh = (1 << 32) // p
-        ra = [(v - ((v * one_sh) >> 32) * p) & MASK for v in A] + [0] * m
-        rb = [(v - ((v * one_sh) >> 32) * p) & MASK for v in B] + [0] * m
+        ra = [red2(red2(v, p2), p2) for v in A] + [0] * m   # a_i < 2^32 < 6p
+        rb = [red2(red2(v, p2), p2) for v in B] + [0] * m
+        assert max(ra + rb) < p2
         fa, fb = fwd(ra), fwd(rb)
         prod = [mont(x, y, p) for x, y in zip(fa, fb)]
         res.append(inv(prod)[:m])

@@ -36,6 +36,24 @@ def swz(u):
     return u ^ (r ^ (r << 1))
 
 
+def xaddr(logn, u):
+    """the kernel's physical word of CTA-wide index u (mul_ntt.cu xbase/xaddr)."""
+    return u + (u >> 4) if logn <= 8 else swz(u)
+
+
+def xaddr_split(logn, lo, T, e):
+    """the kernel's split form: thread base combined with the compile-time e part."""
+    E = e << lo
+    if logn <= 8:
+        base = T + (T >> 4)
+        return base + E + (E >> 4)
+    base = swz(T)
+    hE = swz(E) ^ E
+    if lo >= 5:
+        return (base ^ hE) + E
+    return (base ^ ((E & 31) ^ hE)) + (E & ~31)
+
+
 @pytest.mark.parametrize("logn", range(6, 15))
 def test_pass_groups_and_twiddle_index(logn):
     N = 1 << logn
@@ -61,25 +79,28 @@ def test_pass_groups_and_twiddle_index(logn):
 
 
 @pytest.mark.parametrize("logn", range(6, 15))
-def test_swizzle_bijective_and_conflict_free(logn):
+def test_exchange_addressing_bijective_and_conflict_free(logn):
     N = 1 << logn
     tpi = N >> R_LOG
-    assert sorted(swz(u) for u in range(N)) == list(range(N))
+    ipb = 1 if tpi >= 256 else 256 // tpi
+    span = ipb * N
+    phys = [xaddr(logn, u) for u in range(span)]
+    assert len(set(phys)) == span                                 # injective
+    xw = span + (span >> 4) if logn <= 8 else span
+    assert max(phys) < xw                                         # fits the XW words
     for (_, _, lo) in passes(logn):
-        for w0 in range(0, max(tpi, 32), 32):
-            lanes = [t for t in range(w0, w0 + 32)]
+        for w0 in range(0, min(ipb * tpi, 256), 32):
+            lanes = range(w0, w0 + 32)
             for e in range(16):
-                if tpi >= 32:
-                    banks = {swz(lay(t, e, lo)) % 32 for t in lanes}
-                    assert len(banks) == 32, (logn, lo, e)
-                else:
-                    # several instances per warp: each instance has its own N-word buffer
-                    addrs = {(t // tpi) * N + swz(lay(t % tpi, e, lo)) for t in lanes}
-                    banks = {a % 32 for a in addrs}
-                    # distinct instances' buffers start at multiples of N (>= 64 words):
-                    # conflicts are at most the number of instances sharing a bank
-                    assert len(addrs) == 32
-                    assert max(sum(1 for a in addrs if a % 32 == bk) for bk in banks) <= 32 // tpi
+                addrs = []
+                for t in lanes:
+                    slot, tt = t // tpi, t % tpi
+                    u = slot * N + lay(tt, e, lo)
+                    T = slot * N + ((tt & ((1 << lo) - 1)) | ((tt >> lo) << (lo + 4)))
+                    a = xaddr(logn, u)
+                    assert xaddr_split(logn, lo, T, e) == a              # split form is exact
+                    addrs.append(a)
+                assert len({a % 32 for a in addrs}) == 32, (logn, lo, e)  # no bank conflict
 
 
 @pytest.mark.parametrize("logn", range(6, 15))
