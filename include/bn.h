@@ -122,6 +122,11 @@ uint32_t bn_launches_per_call(int op, uint32_t bits);
  * primitive N-th root for that prime, written to *omega_out.  N = 2^lg_n,
  * lg_n in [6, 14]. */
 void bn_ntt_primes(uint32_t p[3]);
+/* bn_debug_set_grid_cap — tests only: cap every kernel's grid at `cap` CTAs
+ * (0 = default sizing) so small batches exercise the persistent /
+ * grid-stride paths; results must not change (reading R20).
+ * Process-wide, not thread-safe. */
+void bn_debug_set_grid_cap(uint32_t cap);
 bn_status bn_debug_ntt_forward(uint32_t *x, uint64_t n_inst, uint32_t lg_n, int prime,
                                uint32_t *omega_out, bn_stream_t stream);
 

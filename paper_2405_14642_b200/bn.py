@@ -73,6 +73,8 @@ def load():
             lib.bn_ntt_primes.restype = None
             lib.bn_debug_ntt_forward.argtypes = [vp, u64, u32, ctypes.c_int, ctypes.POINTER(u32), vp]
             lib.bn_debug_ntt_forward.restype = ctypes.c_int
+            lib.bn_debug_set_grid_cap.argtypes = [u32]
+            lib.bn_debug_set_grid_cap.restype = None
             _lib = lib
     return _lib
 
@@ -186,6 +188,11 @@ def debug_ntt_forward(x: torch.Tensor, prime: int):
     if st != 0:
         raise BnError(st, "bn_debug_ntt_forward")
     return x, int(om.value)
+
+
+def debug_set_grid_cap(cap: int) -> None:
+    """Tests only: cap every kernel's grid (0 = default)."""
+    load().bn_debug_set_grid_cap(int(cap))
 
 
 def launches_per_call(op: str, bits: int) -> int:

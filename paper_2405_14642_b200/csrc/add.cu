@@ -63,7 +63,7 @@ static cudaError_t launch_add_t(uint32_t* out, const uint32_t* a, const uint32_t
   // resident CTAs per SM for this block size (2048 threads/SM)
   const uint64_t per_sm = 2048 / C::BLOCK;
   const uint64_t cap = (uint64_t)n_sm * per_sm * 8;  // several waves of work per CTA slot
-  const unsigned grid = (unsigned)(n_groups < cap ? n_groups : cap);
+  const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
   add_kernel<LOGM, L><<<grid, C::BLOCK, 0, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
 }

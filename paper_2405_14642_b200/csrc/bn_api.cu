@@ -12,6 +12,10 @@
 #include "../../include/bn.h"
 #include "bn_kernels.h"
 
+namespace bn {
+unsigned g_grid_cap = 0;
+}
+
 namespace {
 
 thread_local int tls_cuda_err = 0;
@@ -383,6 +387,8 @@ uint32_t bn_launches_per_call(int op, uint32_t bits) {
   if (lb < 10 || lb > 18) return 0;
   return 1;
 }
+
+void bn_debug_set_grid_cap(uint32_t cap) { bn::g_grid_cap = cap; }
 
 void bn_ntt_primes(uint32_t p[3]) {
   for (int j = 0; j < 3; j++) p[j] = kPrimes[j];

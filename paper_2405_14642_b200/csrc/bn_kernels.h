@@ -42,6 +42,11 @@ struct NttTables {
 };
 
 // prime constants + per-lg CRT constants -> __constant__ memory of the current device
+// Test knob (bn_debug_set_grid_cap): when > 0, every launcher caps its grid
+// at this many CTAs, forcing the grid-stride / persistent paths on small batches.
+extern unsigned g_grid_cap;
+inline unsigned cap_grid(unsigned g) { return (g_grid_cap && g > g_grid_cap) ? g_grid_cap : g; }
+
 cudaError_t upload_prime_consts(const PrimeConst (&pc)[kNumPrimes], const CrtConst (&crt)[kMaxLogN + 1]);
 
 cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,

@@ -243,7 +243,7 @@ static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t cap = (uint64_t)n_sm * per_sm;  // persistent: one wave of resident CTAs
-  const unsigned grid = (unsigned)(n_groups < cap ? n_groups : cap);
+  const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
   mul_classical_kernel<LOGM, Q><<<grid, C::T, smem, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
 }

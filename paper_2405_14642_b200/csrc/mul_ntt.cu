@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
   extern __shared__ __align__(16) uint32_t sm[];
   const int slot = threadIdx.x / TPI;
   const int t = threadIdx.x % TPI;
-  uint32_t* X = sm + slot * N;                       // exchange buffer, later L | H
+  // this slot's own (padded) exchange region, reused for L | H after the
+  // transforms: it must not reach into another slot's region, because slots
+  // in different warps only synchronise at CTA barriers
+  uint32_t* X = sm + slot * (C::XW / C::IPB);
   uint32_t* Res = sm + C::XW + slot * (3 * M);  // raw inverse outputs per prime
   uint32_t* agg = sm + C::XW + C::IPB * (3 * M);
 
@@ -411,7 +414,7 @@ static cudaError_t launch_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
-  const unsigned grid = (unsigned)(n_groups < cap ? n_groups : cap);
+  const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
   mul_ntt_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw);
   return cudaGetLastError();
 }
@@ -425,7 +428,7 @@ static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const N
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  const unsigned grid = (unsigned)(n_groups < 65535 ? n_groups : 65535);
+  const unsigned grid = cap_grid((unsigned)(n_groups < 65535 ? n_groups : 65535));
   ntt_forward_debug_kernel<LOGN><<<grid, C::T, smem, st>>>(x, n_inst, tb.tw, prime);
   return cudaGetLastError();
 }

@@ -161,10 +161,35 @@ def test_full_size_closed_forms(bits, n):
     _sample_check(a, b, outs, idx)
 
 
+@pytest.mark.parametrize("cap", [1, 3, 7])
+@pytest.mark.parametrize("bits", [1024, 4096, 65536])
+def test_grid_stride_paths(bits, cap):
+    """Results must not depend on the launch configuration (R20): cap the grid
+    so every CTA runs many groups (persistent / double-buffered paths)."""
+    m = bits // 32
+    n = 301 if bits <= 4096 else 9
+    a, b = inputs.make_operands(n, m, seed=cap, cls="MIX")
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    wa, wm = O.add(an, bnp, nthreads=8), O.mul(an, bnp, nthreads=8)
+    da, db = a.to(DEV), b.to(DEV)
+    bn.debug_set_grid_cap(cap)
+    try:
+        got = {k: inputs.to_numpy_u32(f(da, db)) for k, f in OPS.items()}
+    finally:
+        bn.debug_set_grid_cap(0)
+    for k, g in got.items():
+        bad = _first_bad(g, wa if k == "add" else wm)
+        assert bad is None, "%s cap=%d: %s" % (k, cap, bad)
+
+
 def test_classical_equals_ntt_every_size():
+    """Whole paper-sized batches (2^32 bits per operand) at every
+    size: the two multiplication kernels agree on every instance (this is the
+    configuration in which a cross-warp race once showed up, in ~0.5% of the
+    instances of a 2^20 batch, while small batches passed)."""
     for bits in SIZES:
         m = bits // 32
-        n = max(8, (1 << 24) // bits)
+        n = (1 << 32) // bits
         a, b = inputs.make_operands(n, m, seed=9, cls="MIX", device=DEV)
         assert torch.equal(bn.mul_classical(a, b), bn.mul_ntt(a, b)), bits
 

@@ -117,3 +117,21 @@ def test_epilogue_publish_layout(logn):
             assert slot not in writes
             writes[slot] = t
     assert set(writes) == set(range(M))
+
+
+@pytest.mark.parametrize("logn", range(6, 15))
+def test_slot_regions_disjoint(logn):
+    """Each instance slot's exchange addresses stay inside its own region of
+    XW / IPB words, which is also where L | H are published: slots in
+    different warps synchronise only at CTA barriers (mul_ntt.cu, the race
+    fixed after the full-size 4096-bit parity run)."""
+    N = 1 << logn
+    tpi = N >> R_LOG
+    ipb = 1 if tpi >= 256 else 256 // tpi
+    xw = ipb * N + (ipb * N >> 4) if logn <= 8 else ipb * N
+    region = xw // ipb
+    assert region >= N  # room for L | H (N = 2m words)
+    for slot in range(ipb):
+        for u in range(N):
+            a = xaddr(logn, slot * N + u)
+            assert slot * region <= a < (slot + 1) * region
