@@ -58,7 +58,9 @@ def work(bits: int):
     return {
         "add_bytes": 3 * bits // 8,
         "pp": m * (m + 1) // 2,                                  # 32x32 partial products, Eq. 1
-        "modmul": 3 * (3 * (N // 2) * lg + N) + 6 * m,           # Shoup/Montgomery products
+        # 3 primes x (3 transforms x non-trivial twiddle products + N pointwise) + CRT:
+        # a radix-2 transform has (N/2) log2 N butterflies of which N - 1 use w^0 = 1
+        "modmul": 3 * (3 * ((N // 2) * lg - (N - 1)) + N) + 6 * m,
         "u32ops": 300 * m * (m.bit_length() - 1),                # PAPER.md:935 normalisation
     }
 
@@ -200,7 +202,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2405_14642_b200 import bn, inputs
+    from paper_2405_14642_b200 import bn, inputs, shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -215,17 +217,13 @@ def main():
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return shard.max_over_ranks(x, dist if world > 1 else None, dev)
 
     peaks = load_peaks()
     bits = args.bits
     m = bits // 32
     n = args.n_inst or (1 << 32) // bits
-    inst0 = rank * n  # weak scaling: rank r owns global instances [r n, (r+1) n)
+    inst0, _ = shard.weak_range(rank, world, n)  # weak scaling: rank r owns [r n, (r+1) n)
     bn.prepare(local)
     a, b = inputs.make_operands(n, m, seed=args.seed, cls=args.cls, inst0=inst0, device=dev)
     o_add, o_mc, o_mn = torch.empty_like(a), torch.empty_like(a), torch.empty_like(a)
@@ -303,7 +301,8 @@ def main():
         ach = n * w["modmul"] / (op_ms["mul_ntt"] * 1e-3) / 1e12
         roof = {"kernel": "mul_ntt_kernel", "bound": "alu", "achieved": ach,
                 "peak": N_SM * MODMUL_PER_CLK_SM * f_ghz / 1e3, "unit": "Tmodmul/s",
-                "per_unit": "3*(3*(N/2)*log2 N + N) + 6m modular products per instance (N = 2m); "
+                "per_unit": "3*(3*((N/2)*log2 N - (N-1)) + N) + 6m modular products per instance "
+                            "(N = 2m; non-trivial twiddles, pointwise, CRT); "
                             "peak = 148 SM x 16 modmul/clk (4 FMA-pipe slots each) x sm_max_mhz"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_source"] = peaks["source"] if roof["bound"] == "hbm" else \
