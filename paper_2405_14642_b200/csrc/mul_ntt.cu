@@ -81,7 +81,8 @@ struct NttCfg {
   static constexpr int T = IPB * TPI;
   // exchange area (padded by 1/16 for LOGN <= 8, see xbase), raw residues, agg
   static constexpr int XW = LOGN <= 8 ? IPB * N + (IPB * N >> 4) : IPB * N;
-  static constexpr int SMEM_WORDS = XW + IPB * 3 * M + T / 32;
+  // two exchange planes (A and B are transformed together), raw residues, agg
+  static constexpr int SMEM_WORDS = 2 * XW + IPB * (3 * M + (TPI < 32 ? 16 : 0)) + T / 32;
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
   static constexpr int MINB = T <= 256 ? (LOGN <= 8 ? 4 : 3) : 1;
 };
@@ -112,8 +113,12 @@ BN_DEV void bar() {
   else __syncthreads();
 }
 
-template <int LOGN, int P, bool PADDED>
-BN_DEV void fwd_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
+// One forward register pass on NV vectors at once (NV = 2: A and B are
+// transformed together — every twiddle load serves both, and the two
+// independent dependency chains double the ILP at the register cost the
+// held A-hat used to have).
+template <int LOGN, int P, bool PADDED, int NV>
+BN_DEV void fwd_pass(uint32_t (&x)[NV][16], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
   using PS = PassCfg<LOGN, P>;
   const int tlow = t & ((1 << PS::LO) - 1);
 #pragma unroll
@@ -127,17 +132,23 @@ BN_DEV void fwd_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uin
       if (PS::LO == 0 && el == 0) {
         // twiddle w^0 = 1 (exponent j = tlow + el << LO = 0 for every thread):
         // no multiplication, only the lazy reductions
-        const uint32_t xs = x[e], ys = x[e | (1 << b)];
-        x[e] = red2(xs + ys, p2);
-        x[e | (1 << b)] = red2(xs - ys + p2, p2);
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+          const uint32_t xs = x[v][e], ys = x[v][e | (1 << b)];
+          x[v][e] = red2(xs + ys, p2);
+          x[v][e | (1 << b)] = red2(xs - ys + p2, p2);
+        }
         continue;
       }
       const uint2 w = __ldg(Ts + (el << PS::LO));
-      if (PADDED && P == 0 && s == 0) {
-        // zero-padded input: x[e | 8] == 0, so (x + 0, (x - 0) w)
-        x[e | (1 << b)] = shoup(x[e], w.x, w.y, p);
-      } else {
-        gs_bfly(x[e], x[e | (1 << b)], w, p, p2);
+#pragma unroll
+      for (int v = 0; v < NV; v++) {
+        if (PADDED && P == 0 && s == 0) {
+          // zero-padded input: x[e | 8] == 0, so (x + 0, (x - 0) w)
+          x[v][e | (1 << b)] = shoup(x[v][e], w.x, w.y, p);
+        } else {
+          gs_bfly(x[v][e], x[v][e | (1 << b)], w, p, p2);
+        }
       }
     }
   }
@@ -195,53 +206,63 @@ BN_DEV int xaddr(int base, int e) {
   }
 }
 
-template <int LOGN, int LO_FROM, int LO_TO, int TPI>
-BN_DEV void xchg(uint32_t (&x)[16], uint32_t* X0, int xo, int t) {
+// Exchange NV register vectors between pass layouts; vector v uses the plane
+// X0 + v * PLANE (PLANE = the CTA's exchange-area size XW).
+template <int LOGN, int LO_FROM, int LO_TO, int TPI, int NV, int PLANE>
+BN_DEV void xchg(uint32_t (&x)[NV][16], uint32_t* X0, int xo, int t) {
   bar<TPI>();  // previous readers of X are done
   const int bw = xbase<LOGN, LO_FROM>(xo, t);
 #pragma unroll
-  for (int e = 0; e < 16; e++) X0[xaddr<LOGN, LO_FROM>(bw, e)] = x[e];
+  for (int v = 0; v < NV; v++)
+#pragma unroll
+    for (int e = 0; e < 16; e++) X0[v * PLANE + xaddr<LOGN, LO_FROM>(bw, e)] = x[v][e];
   bar<TPI>();
   const int br = xbase<LOGN, LO_TO>(xo, t);
 #pragma unroll
-  for (int e = 0; e < 16; e++) x[e] = X0[xaddr<LOGN, LO_TO>(br, e)];
+  for (int v = 0; v < NV; v++)
+#pragma unroll
+    for (int e = 0; e < 16; e++) x[v][e] = X0[v * PLANE + xaddr<LOGN, LO_TO>(br, e)];
 }
 
-template <int LOGN, bool PADDED>
-BN_DEV void fwd_all(uint32_t (&x)[16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p, uint32_t p2) {
+template <int LOGN, bool PADDED, int NV>
+BN_DEV void fwd_all(uint32_t (&x)[NV][16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p,
+                    uint32_t p2) {
   using C = NttCfg<LOGN>;
-  fwd_pass<LOGN, 0, PADDED>(x, t, tw, p, p2);
+  constexpr int PL = C::XW;
+  fwd_pass<LOGN, 0, PADDED, NV>(x, t, tw, p, p2);
   if constexpr (C::NP > 1) {
-    xchg<LOGN, PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X0, xo, t);
-    fwd_pass<LOGN, 1, PADDED>(x, t, tw, p, p2);
+    xchg<LOGN, PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, C::TPI, NV, PL>(x, X0, xo, t);
+    fwd_pass<LOGN, 1, PADDED, NV>(x, t, tw, p, p2);
   }
   if constexpr (C::NP > 2) {
-    xchg<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X0, xo, t);
-    fwd_pass<LOGN, 2, PADDED>(x, t, tw, p, p2);
+    xchg<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, C::TPI, NV, PL>(x, X0, xo, t);
+    fwd_pass<LOGN, 2, PADDED, NV>(x, t, tw, p, p2);
   }
   if constexpr (C::NP > 3) {
-    xchg<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, C::TPI>(x, X0, xo, t);
-    fwd_pass<LOGN, 3, PADDED>(x, t, tw, p, p2);
+    xchg<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, C::TPI, NV, PL>(x, X0, xo, t);
+    fwd_pass<LOGN, 3, PADDED, NV>(x, t, tw, p, p2);
   }
   static_assert(C::NP <= 4, "LOGN <= 16");
 }
 
 template <int LOGN>
-BN_DEV void inv_all(uint32_t (&x)[16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p, uint32_t p2) {
+BN_DEV void inv_all(uint32_t (&x1)[16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p, uint32_t p2) {
   using C = NttCfg<LOGN>;
+  constexpr int PL = C::XW;
+  uint32_t(&x)[1][16] = reinterpret_cast<uint32_t(&)[1][16]>(x1);
   if constexpr (C::NP > 3) {
-    inv_pass<LOGN, 3>(x, t, tw, p, p2);
-    xchg<LOGN, PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, C::TPI>(x, X0, xo, t);
+    inv_pass<LOGN, 3>(x1, t, tw, p, p2);
+    xchg<LOGN, PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, C::TPI, 1, PL>(x, X0, xo, t);
   }
   if constexpr (C::NP > 2) {
-    inv_pass<LOGN, 2>(x, t, tw, p, p2);
-    xchg<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, C::TPI>(x, X0, xo, t);
+    inv_pass<LOGN, 2>(x1, t, tw, p, p2);
+    xchg<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, C::TPI, 1, PL>(x, X0, xo, t);
   }
   if constexpr (C::NP > 1) {
-    inv_pass<LOGN, 1>(x, t, tw, p, p2);
-    xchg<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, C::TPI>(x, X0, xo, t);
+    inv_pass<LOGN, 1>(x1, t, tw, p, p2);
+    xchg<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, C::TPI, 1, PL>(x, X0, xo, t);
   }
-  inv_pass<LOGN, 0>(x, t, tw, p, p2);
+  inv_pass<LOGN, 0>(x1, t, tw, p, p2);
 }
 
 // 3-word accumulate (a0, a1, a2) += (c0, c1, c2)
@@ -265,8 +286,11 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
   // transforms: it must not reach into another slot's region, because slots
   // in different warps only synchronise at CTA barriers
   uint32_t* X = sm + slot * (C::XW / C::IPB);
-  uint32_t* Res = sm + C::XW + slot * (3 * M);  // raw inverse outputs per prime
-  uint32_t* agg = sm + C::XW + C::IPB * (3 * M);
+  // raw inverse outputs per prime; per-slot stride padded by 16 words so the two
+  // instances sharing a warp (TPI = 16) write different banks
+  constexpr int RS = 3 * M + (C::TPI < 32 ? 16 : 0);
+  uint32_t* Res = sm + 2 * C::XW + slot * RS;
+  uint32_t* agg = sm + 2 * C::XW + C::IPB * RS;
 
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
@@ -280,30 +304,25 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
       const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
       const uint2* twf = tw + (2 * j + 0) * (N - 1);
       const uint2* twi = tw + (2 * j + 1) * (N - 1);
-      uint32_t x[16], ah[16];
-#pragma unroll 1
-      for (int op = 0; op < 2; op++) {
-        // N-1: reduce the limbs mod p into pass-0 layout (index t + e N/16),
-        // upper half is the zero padding (reading R11)
-        const uint32_t* src = op == 0 ? ai : bi;
+      uint32_t xab[2][16];
+      // N-1: reduce the limbs mod p into pass-0 layout (index t + e N/16),
+      // upper half is the zero padding (reading R11)
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
-          const uint32_t v = valid ? __ldg(src + t + e * (N / 16)) : 0u;
-          // a_i < 2^32 < 4p + 2p: two conditional subtractions of 2p -> [0, 2p)
-          x[e] = red2(red2(v, p2), p2);
-        }
-#pragma unroll
-        for (int e = 8; e < 16; e++) x[e] = 0u;
-        // N-2: forward transform
-        fwd_all<LOGN, true>(x, sm, slot * N, t, twf, p, p2);
-        if (op == 0) {
-#pragma unroll
-          for (int e = 0; e < 16; e++) ah[e] = x[e];
-        }
+      for (int e = 0; e < 8; e++) {
+        const uint32_t va = valid ? __ldg(ai + t + e * (N / 16)) : 0u;
+        const uint32_t vb = valid ? __ldg(bi + t + e * (N / 16)) : 0u;
+        // a_i < 2^32 < 6p: two conditional subtractions of 2p -> [0, 2p)
+        xab[0][e] = red2(red2(va, p2), p2);
+        xab[1][e] = red2(red2(vb, p2), p2);
       }
-      // N-3: pointwise product (same register layout for A-hat and B-hat)
 #pragma unroll
-      for (int e = 0; e < 16; e++) x[e] = mont(ah[e], x[e], p, pinv);
+      for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
+      // N-2: forward transforms of A and B together
+      fwd_all<LOGN, true, 2>(xab, sm, slot * N, t, twf, p, p2);
+      // N-3: pointwise product (same register layout for A-hat and B-hat)
+      uint32_t x[16];
+#pragma unroll
+      for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[1][e], p, pinv);
       // N-4: inverse transform -> pass-0 layout, natural order
       inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
       // keep coefficients 0..M-1 (truncated product): e < 8
@@ -387,14 +406,14 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T)
     const bool valid = inst < n_inst;
     uint32_t* row = xg + (valid ? inst : 0) * N;
     const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2;
-    uint32_t x[16];
+    uint32_t x[1][16];
 #pragma unroll
-    for (int e = 0; e < 16; e++) x[e] = valid ? row[t + e * (N / 16)] : 0u;
-    fwd_all<LOGN, false>(x, sm, slot * N, t, tw + 2 * j * (N - 1), p, p2);
+    for (int e = 0; e < 16; e++) x[0][e] = valid ? row[t + e * (N / 16)] : 0u;
+    fwd_all<LOGN, false, 1>(x, sm, slot * N, t, tw + 2 * j * (N - 1), p, p2);
     constexpr int LO_LAST = PassCfg<LOGN, C::NP - 1>::LO;
     if (valid) {
 #pragma unroll
-      for (int e = 0; e < 16; e++) row[lay<LO_LAST>(t, e)] = red2(x[e], p);
+      for (int e = 0; e < 16; e++) row[lay<LO_LAST>(t, e)] = red2(x[0][e], p);
     }
     __syncthreads();
   }

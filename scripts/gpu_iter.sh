@@ -14,6 +14,6 @@ for k, v in d['ops'].items(): print(' ', k, {a: round(b, 4) for a, b in v.items(
 print('  roofline', d['roofline']['kernel'], round(d['roofline']['frac'], 3), 'clocks', d['clocks'])
 "
 for k in ${KERNELS:-mul_ntt_kernel mul_classical_kernel}; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
+  timeout 900 ncu --set full --metrics sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fmaheavy.sum --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
     -o gpurun_out/prof_${k}_$tag python bench.py --no-e2e --no-cpu --steps 1 --warmup 3 > gpurun_out/ncu_${k}_$tag.log 2>&1; echo ncu_${k}_rc=$?
 done
