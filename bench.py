@@ -307,7 +307,7 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_source"] = peaks["source"] if roof["bound"] == "hbm" else \
         "derived: measured int-pipe rates (profiles/r01_int_peak.jsonl) x sm_max_mhz"
-    roof["traffic"] = load_traffic(dom, bits)
+    roof["traffic"] = load_traffic(roof["kernel"], bits)
 
     line = {
         "metric": METRIC, "value": value, "unit": "mults/s", "n_gpus": world, "steps": args.steps,
@@ -359,8 +359,9 @@ def main():
 
 
 def load_traffic(kernel: str, bits: int):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/ncu_traffic.json), if one matches."""
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
+    the dominant kernel from the committed ncu --set full capture at this
+    size (profiles/ncu_traffic.json, key "<kernel>@<bits>"), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
