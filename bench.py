@@ -21,6 +21,9 @@ Printed (rank 0): one JSON line.
 
 `--impl reference` times the oracle itself (the CPU reference arm).
 `--sweep` additionally prints one line per (op, size) for 1K..256K bits.
+The fused NEXT-row workloads (6-Add, Poly with either multiplication) are
+timed after the step on the same inputs and reported under "ops" (not in
+`value`, which is the §8(a) step); `--no-fused` skips them.
 """
 from __future__ import annotations
 
@@ -192,6 +195,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also print per-(op, size) lines")
+    ap.add_argument("--no-fused", action="store_true", help="skip the 6-Add / Poly timings")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -283,6 +287,9 @@ def main():
                     "Gu32ops/s": total_inst * w["u32ops"] / (op_ms["mul_ntt"] * 1e-3) / 1e9},
     }
     clocks = sampler.result()
+    if not args.no_fused:
+        ops.update(time_fused(bn, torch, a, b, o_add, stream, args.steps, n, world, w, max_over_ranks,
+                              barrier))
 
     # roofline of the dominant kernel (per-GPU work / per-launch time)
     dom = max(op_ms, key=op_ms.get)
@@ -358,6 +365,45 @@ def main():
     return 0
 
 
+def fused_rates(name: str, ms: float, total_inst: int, w):
+    """Rates of the paper's fused workloads: 6-Add in GB/s
+    over 3*bits/8 bytes (the footnote's ideal: read a, b, write one result);
+    Poly as 4 multiplications (mults/s) and 4x the 1-Mul Gu32ops count."""
+    r = {"ms": ms}
+    if name == "add6":
+        r["GB/s"] = total_inst * w["add_bytes"] / (ms * 1e-3) / 1e9
+        r["add6/s"] = total_inst / (ms * 1e-3)
+    else:
+        r["poly/s"] = total_inst / (ms * 1e-3)
+        r["mults/s"] = 4 * total_inst / (ms * 1e-3)
+        r["Gu32ops/s"] = 4 * total_inst * w["u32ops"] / (ms * 1e-3) / 1e9
+    return r
+
+
+def time_fused(bn, torch, a, b, out, stream, steps, n, world, w, max_over_ranks, barrier):
+    """NEXT rows, timed after the step on the same inputs:
+    each op `steps` times back to back, CUDA events on the launch stream."""
+    fns = {"add6": lambda: bn.add6(a, b, out=out)}
+    for name, f in (("poly_classical", bn.poly_classical), ("poly_ntt", bn.poly_ntt)):
+        ws = bn.poly_workspace(name, a)
+        fns[name] = (lambda f=f, ws=ws: f(a, b, out=out, workspace=ws))
+    res = {}
+    for name, f in fns.items():
+        for _ in range(2):
+            f()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            f()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+        res[name] = fused_rates(name, ms, n * world, w)
+    return res
+
+
 def load_traffic(kernel: str, bits: int):
     """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
     the dominant kernel from the committed ncu --set full capture at this
@@ -380,8 +426,15 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
         a, b = inputs.make_operands(n, m, seed=args.seed, cls=args.cls, inst0=rank * n, device=dev)
         o = torch.empty_like(a)
         w = work(bits)
-        for name, f in (("add", bn.add), ("mul_classical", bn.mul_classical), ("mul_ntt", bn.mul_ntt)):
-            reps = 20 if name != "mul_classical" or bits <= 32768 else 3
+        fns = [("add", bn.add), ("mul_classical", bn.mul_classical), ("mul_ntt", bn.mul_ntt)]
+        if not args.no_fused:
+            wsc, wsn = bn.poly_workspace("poly_classical", a), bn.poly_workspace("poly_ntt", a)
+            fns += [("add6", bn.add6),
+                    ("poly_classical", lambda x, y, out: bn.poly_classical(x, y, out=out, workspace=wsc)),
+                    ("poly_ntt", lambda x, y, out: bn.poly_ntt(x, y, out=out, workspace=wsn))]
+        for name, f in fns:
+            slow = name in ("mul_classical", "poly_classical") and bits > 32768
+            reps = 3 if slow else 20
             for _ in range(2):
                 f(a, b, out=o)
             barrier()
@@ -395,7 +448,11 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
             ms = max_over_ranks(e0.elapsed_time(e1) / reps)
             tot = n * world
             row = {"sweep": True, "op": name, "bits": bits, "instances": tot, "ms": ms, "n_gpus": world}
-            if name == "add":
+            if name in ("add6", "poly_classical", "poly_ntt"):
+                row.update(fused_rates(name, ms, tot, w))
+                if name == "add6":
+                    row["frac_hbm"] = row["GB/s"] / world / peaks["hbm_gbs"]
+            elif name == "add":
                 row["GB/s"] = tot * w["add_bytes"] / (ms * 1e-3) / 1e9
                 row["frac_hbm"] = row["GB/s"] / world / peaks["hbm_gbs"]
             else:

@@ -87,6 +87,49 @@ bn_status bn_mul_classical(void *out, const void *a, const void *b, uint64_t n_i
 bn_status bn_mul_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
                      uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
 
+/* ---- fused workloads (block-level fusion) ---------------
+ * The paper's 6-Add and Poly benchmarks (Tables 1 and 2): several dependent
+ * operations per instance inside ONE kernel, intermediates kept on chip (or,
+ * for Poly, in a small per-CTA workspace that stays in L2), so that a batch
+ * reads a and b once and writes one result ("both programs read two
+ * integers from global memory and write one as result"
+ * footnote).  Same layout, sizes, alignment, aliasing, stream and error
+ * rules as bn_add.
+ *
+ * bn_add6 — out[k] = (4 a[k] + 3 b[k]) mod 2^bits computed as six dependent
+ * scan-additions r = a + b, r += a, r += b, r += a, r += b, r += a (6-Add,
+ * PAPER.md:917-918; the paper does not print the expression: DESIGN.md
+ * reading R17).
+ */
+bn_status bn_add6(void *out, const void *a, const void *b, uint64_t n_inst,
+                  uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
+
+/*
+ * bn_poly_classical / bn_poly_ntt — out[k] = ((a a + b)(b b + b) + a b)
+ * mod 2^bits (Poly, PAPER.md:918 and the Table 2 caption: "four
+ * multiplications and two additions"; the expression has three, all are
+ * computed — DESIGN.md reading R18), with every multiplication done by the
+ * classical (bn_mul_classical) or NTT (bn_mul_ntt) algorithm and each
+ * addition fused into the epilogue of the product before it.
+ * workspace: DEVICE buffer of at least bn_poly_workspace_bytes(op, n_inst,
+ * n_limbs, limb_bits) bytes on the current device, 16-byte aligned, owned
+ * by the caller, not overlapping a, b or out; its contents are scratch
+ * (undefined after the call) and it must not be used by another call that
+ * may run concurrently.  Too small -> BN_EINVAL, nothing launched.
+ */
+bn_status bn_poly_classical(void *out, const void *a, const void *b, uint64_t n_inst,
+                            uint32_t n_limbs, uint32_t limb_bits, void *workspace,
+                            uint64_t workspace_bytes, bn_stream_t stream);
+bn_status bn_poly_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
+                      uint32_t n_limbs, uint32_t limb_bits, void *workspace,
+                      uint64_t workspace_bytes, bn_stream_t stream);
+
+/* Workspace bytes a bn_poly_* call needs on the CURRENT device for this
+ * batch (one slice of 3 intermediates per resident CTA; <= 3 * n_inst *
+ * bits / 8).  op = BN_OP_POLY_CLASSICAL or BN_OP_POLY_NTT.  Returns 0 for
+ * n_inst == 0 or invalid arguments.  May initialise the device (bn_prepare). */
+uint64_t bn_poly_workspace_bytes(int op, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
+
 /* Build the NTT twiddle/CRT tables for `device` (all sizes), synchronously.
  * Idempotent and thread-safe; bn_mul_ntt calls it lazily. */
 bn_status bn_prepare(int device);
@@ -96,12 +139,14 @@ bn_status bn_prepare(int device);
  * is cut into chunks that are copied host->device, processed by each op in
  * `ops` (same operands a, b), and copied device->host into outs[i], with
  * copies and kernels overlapped on two streams of the current device.
- * ops[i] is one of BN_OP_ADD / BN_OP_MUL_CLASSICAL / BN_OP_MUL_NTT;
+ * ops[i] is one of the BN_OP_* codes below (Poly ops get their workspace
+ * from the pipeline's own scratch);
  * outs[i] is a host buffer of n_inst*n_limbs limbs.  Host buffers should be
  * page-locked (cudaHostAlloc / torch pin_memory) for full bandwidth.
  * Device scratch is allocated on first use and cached per device (grown on
  * demand).  Synchronous: returns when every output is in host memory. */
-enum { BN_OP_ADD = 0, BN_OP_MUL_CLASSICAL = 1, BN_OP_MUL_NTT = 2 };
+enum { BN_OP_ADD = 0, BN_OP_MUL_CLASSICAL = 1, BN_OP_MUL_NTT = 2, BN_OP_ADD6 = 3,
+       BN_OP_POLY_CLASSICAL = 4, BN_OP_POLY_NTT = 5 };
 bn_status bn_run_host(const int *ops, void *const *outs, int n_ops, const void *a,
                       const void *b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
 

@@ -80,9 +80,35 @@ void oracle_mul_full(uint32_t *out2m, const uint32_t *a, const uint32_t *b, uint
     }
 }
 
+/* ---- the paper's fused workloads, as plain compositions ----
+ * 6-Add (Table 1): six dependent additions; the paper does
+ * not print the expression, reading R17: r = a + b, then
+ * alternately + a, + b (r = 4a + 3b mod 2^(32m)).
+ * Poly (Table 2 caption): (a*a + b) * (b*b + b) + a*b,
+ * mod 2^(32m), evaluated exactly in that order with the functions above.
+ * tmp: 4m scratch words.  out may not alias a or b. */
+void oracle_add6(uint32_t *out, const uint32_t *a, const uint32_t *b, uint32_t m)
+{
+    oracle_add(out, a, b, m);                 /* a + b */
+    for (int k = 1; k < 6; k++)               /* + a, + b, + a, + b, + a */
+        oracle_add(out, out, (k & 1) ? a : b, m);
+}
+
+void oracle_poly(uint32_t *out, const uint32_t *a, const uint32_t *b, uint32_t m, uint32_t *tmp)
+{
+    uint32_t *aa = tmp, *bb = tmp + m, *t1 = tmp + 2 * (size_t)m, *t2 = tmp + 3 * (size_t)m;
+    oracle_mul(aa, a, a, m);                  /* a * a         */
+    oracle_add(t1, aa, b, m);                 /* a * a + b     */
+    oracle_mul(bb, b, b, m);                  /* b * b         */
+    oracle_add(t2, bb, b, m);                 /* b * b + b     */
+    oracle_mul(out, t1, t2, m);               /* (..) * (..)   */
+    oracle_mul(aa, a, b, m);                  /* a * b         */
+    oracle_add(out, out, aa, m);              /* ... + a * b   */
+}
+
 /* ---- batch wrappers: instance-major [n_inst][m], one call per instance ---- */
 
-enum { ORACLE_ADD = 0, ORACLE_MUL = 1 };
+enum { ORACLE_ADD = 0, ORACLE_MUL = 1, ORACLE_ADD6 = 2, ORACLE_POLY = 3 };
 
 typedef struct {
     int op;
@@ -101,6 +127,12 @@ static void *run_job(void *arg)
         uint32_t *oi = j->out + i * j->m;
         if (j->op == ORACLE_ADD) {
             oracle_add(oi, ai, bi, j->m);
+        } else if (j->op == ORACLE_ADD6) {
+            oracle_add6(oi, ai, bi, j->m);
+        } else if (j->op == ORACLE_POLY) {
+            if (!tmp) tmp = (uint32_t *)malloc((size_t)5 * j->m * sizeof(uint32_t));
+            oracle_poly(tmp + 4 * (size_t)j->m, ai, bi, j->m, tmp);
+            memcpy(oi, tmp + 4 * (size_t)j->m, (size_t)j->m * sizeof(uint32_t));
         } else {
             /* oracle_mul may not alias: go through a scratch buffer */
             if (!tmp) tmp = (uint32_t *)malloc((size_t)j->m * sizeof(uint32_t));
@@ -117,7 +149,7 @@ static void *run_job(void *arg)
 int oracle_batch(int op, uint32_t *out, const uint32_t *a, const uint32_t *b,
                  uint64_t n_inst, uint32_t m, int nthreads)
 {
-    if (op != ORACLE_ADD && op != ORACLE_MUL) return -1;
+    if (op < ORACLE_ADD || op > ORACLE_POLY) return -1;
     if (nthreads <= 1 || n_inst < 2) {
         job_t j = {op, out, a, b, 0, n_inst, m};
         run_job(&j);

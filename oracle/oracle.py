@@ -13,6 +13,8 @@ little-endian limbs):
 * ``add(a, b)``       -> (A + B) mod 2^(32m)   (Fig. 1 left)
 * ``mul(a, b)``       -> (A * B) mod 2^(32m)   (Eq. 1)
 * ``mul_full(a, b)``  -> A * B as 2m limbs (for residue pins)
+* ``add6(a, b)``      -> 6-Add, 4A + 3B mod 2^(32m) as six additions (R17)
+* ``poly(a, b)``      -> Poly, ((A A + B)(B B + B) + A B) mod 2^(32m)
 * ``add_carry(a, b)`` -> (sum, carry-out) of one instance (carry for tests)
 """
 from __future__ import annotations
@@ -32,6 +34,8 @@ _lib = None
 
 ORACLE_ADD = 0
 ORACLE_MUL = 1
+ORACLE_ADD6 = 2
+ORACLE_POLY = 3
 
 
 def build(force: bool = False) -> str:
@@ -92,6 +96,16 @@ def add(a, b, nthreads: int = 1) -> np.ndarray:
 def mul(a, b, nthreads: int = 1) -> np.ndarray:
     """(A * B) mod 2^(32m) per instance (rows)."""
     return _batch(ORACLE_MUL, a, b, nthreads)
+
+
+def add6(a, b, nthreads: int = 1) -> np.ndarray:
+    """6-Add: r = a + b, then + a, + b, + a, + b, + a, per instance (rows)."""
+    return _batch(ORACLE_ADD6, a, b, nthreads)
+
+
+def poly(a, b, nthreads: int = 1) -> np.ndarray:
+    """Poly: ((a a + b)(b b + b) + a b) mod 2^(32m) per instance (rows)."""
+    return _batch(ORACLE_POLY, a, b, nthreads)
 
 
 def add_carry(a, b):

@@ -27,8 +27,9 @@ SUPPORTED_BITS = tuple(1 << k for k in range(10, 19))
 _STATUS = {0: "BN_OK", 1: "BN_EINVAL", 2: "BN_ESIZE", 3: "BN_EALIGN", 4: "BN_EALIAS",
            5: "BN_ECUDA", 6: "BN_ENODEV"}
 
-OP_ADD, OP_MUL_CLASSICAL, OP_MUL_NTT = 0, 1, 2
-OPS = {"add": OP_ADD, "mul_classical": OP_MUL_CLASSICAL, "mul_ntt": OP_MUL_NTT}
+OP_ADD, OP_MUL_CLASSICAL, OP_MUL_NTT, OP_ADD6, OP_POLY_CLASSICAL, OP_POLY_NTT = 0, 1, 2, 3, 4, 5
+OPS = {"add": OP_ADD, "mul_classical": OP_MUL_CLASSICAL, "mul_ntt": OP_MUL_NTT, "add6": OP_ADD6,
+       "poly_classical": OP_POLY_CLASSICAL, "poly_ntt": OP_POLY_NTT}
 
 
 class BnError(RuntimeError):
@@ -53,10 +54,16 @@ def load():
                 raise ImportError("libbn.so not built at %s — run __graft_entry__.build()" % _LIB_PATH)
             lib = ctypes.CDLL(_LIB_PATH)
             vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
-            for name in ("bn_add", "bn_mul_classical", "bn_mul_ntt"):
+            for name in ("bn_add", "bn_mul_classical", "bn_mul_ntt", "bn_add6"):
                 f = getattr(lib, name)
                 f.argtypes = [vp, vp, vp, u64, u32, u32, vp]
                 f.restype = ctypes.c_int
+            for name in ("bn_poly_classical", "bn_poly_ntt"):
+                f = getattr(lib, name)
+                f.argtypes = [vp, vp, vp, u64, u32, u32, vp, u64, vp]
+                f.restype = ctypes.c_int
+            lib.bn_poly_workspace_bytes.argtypes = [ctypes.c_int, u64, u32, u32]
+            lib.bn_poly_workspace_bytes.restype = u64
             lib.bn_prepare.argtypes = [ctypes.c_int]
             lib.bn_prepare.restype = ctypes.c_int
             lib.bn_run_host.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp), ctypes.c_int,
@@ -135,6 +142,50 @@ def mul_classical(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
 def mul_ntt(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
     """(a * b) mod 2^bits per instance, exact 3-prime NTT (bn_mul_ntt)."""
     return _call("bn_mul_ntt", a, b, out)
+
+
+def add6(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    """6-Add: (4a + 3b) mod 2^bits as six fused scan-additions (bn_add6)."""
+    return _call("bn_add6", a, b, out)
+
+
+def poly_workspace_bytes(op: str, n_inst: int, n_limbs: int, limb_bits: int = 32) -> int:
+    """Workspace bytes bn_poly_* needs on the current device."""
+    return int(load().bn_poly_workspace_bytes(OPS[op], n_inst, n_limbs, limb_bits))
+
+
+def poly_workspace(op: str, a: torch.Tensor) -> torch.Tensor:
+    """A workspace tensor for poly_* on a's device (reusable across calls on one stream)."""
+    with torch.cuda.device(a.device):
+        nb = poly_workspace_bytes(op, a.shape[0], a.shape[1], _limb_bits(a))
+    return torch.empty(max(16, nb), dtype=torch.uint8, device=a.device)
+
+
+def _poly(name: str, op: str, a, b, out, workspace):
+    out = _check(a, b, out)
+    if workspace is None:
+        workspace = poly_workspace(op, a)
+    if not workspace.is_cuda or workspace.device != a.device or not workspace.is_contiguous():
+        raise ValueError("workspace must be a contiguous CUDA tensor on the operands' device")
+    lib = load()
+    n_inst, n_limbs = a.shape
+    with torch.cuda.device(a.device):
+        stream = torch.cuda.current_stream(a.device).cuda_stream
+        st = getattr(lib, name)(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs, _limb_bits(a),
+                                workspace.data_ptr(), workspace.numel() * workspace.element_size(), stream)
+    if st != 0:
+        raise BnError(st, name)
+    return out
+
+
+def poly_classical(a: torch.Tensor, b: torch.Tensor, out=None, workspace=None) -> torch.Tensor:
+    """Poly: ((a a + b)(b b + b) + a b) mod 2^bits, classical products, one kernel."""
+    return _poly("bn_poly_classical", "poly_classical", a, b, out, workspace)
+
+
+def poly_ntt(a: torch.Tensor, b: torch.Tensor, out=None, workspace=None) -> torch.Tensor:
+    """Poly: ((a a + b)(b b + b) + a b) mod 2^bits, NTT products, one kernel."""
+    return _poly("bn_poly_ntt", "poly_ntt", a, b, out, workspace)
 
 
 def prepare(device: int = 0) -> None:

@@ -54,6 +54,58 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
   }
 }
 
+// 6-Add (Table 1): six dependent additions fused in one
+// kernel with every intermediate held in registers (block-level fusion).
+// The paper does not print the expression; reading R17:
+// r = a + b, then alternately + a, + b, i.e. r = 4a + 3b mod 2^bits — six
+// full carry scans, each one the §2 map -> scan -> map.  The two agg
+// buffers alternate so consecutive scans need no extra barrier (a scan's
+// own __syncthreads orders every thread's previous read of the other buffer).
+template <int LOGM, int L>
+__global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
+    add6_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
+                const uint32_t* __restrict__ b, uint64_t n_inst) {
+  using C = AddCfg<LOGM, L>;
+  __shared__ uint32_t agg[2][C::BLOCK / 32];
+  const uint32_t slot = threadIdx.x / C::TPI;
+  const uint32_t lt = threadIdx.x % C::TPI;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t inst = grp * C::IPB + slot;
+    const bool valid = inst < n_inst;
+    const uint64_t off = inst * (uint64_t)C::M + (uint64_t)lt * L;
+    uint32_t x[L], y[L], r[L], s[L];
+    if (valid) {
+      load_limbs<L>(x, a + off);
+      load_limbs<L>(y, b + off);
+    } else {
+#pragma unroll
+      for (int i = 0; i < L; i++) x[i] = y[i] = 0;
+    }
+    add_regs<L, C::TPI>(x, y, r, valid, agg[0]);  // a + b
+    add_regs<L, C::TPI>(r, x, s, valid, agg[1]);  // + a
+    add_regs<L, C::TPI>(s, y, r, valid, agg[0]);  // + b
+    add_regs<L, C::TPI>(r, x, s, valid, agg[1]);  // + a
+    add_regs<L, C::TPI>(s, y, r, valid, agg[0]);  // + b
+    add_regs<L, C::TPI>(r, x, s, valid, agg[1]);  // + a
+    if (valid) store_limbs<L>(out + off, s);
+    if constexpr (C::TPI > 32) __syncthreads();
+  }
+}
+
+template <int LOGM>
+static cudaError_t launch_add6_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                 cudaStream_t st, int n_sm) {
+  constexpr int L = 8;
+  using C = AddCfg<LOGM, L>;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  const uint64_t per_sm = 2048 / C::BLOCK;
+  const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
+  const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
+  add6_kernel<LOGM, L><<<grid, C::BLOCK, 0, st>>>(out, a, b, n_inst);
+  return cudaGetLastError();
+}
+
 template <int LOGM>
 static cudaError_t launch_add_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                 cudaStream_t st, int n_sm) {
@@ -80,6 +132,22 @@ cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_
     case 11: return launch_add_t<11>(out, a, b, n_inst, st, n_sm);
     case 12: return launch_add_t<12>(out, a, b, n_inst, st, n_sm);
     case 13: return launch_add_t<13>(out, a, b, n_inst, st, n_sm);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_add6(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                        cudaStream_t st, int n_sm) {
+  switch (logm) {
+    case 5: return launch_add6_t<5>(out, a, b, n_inst, st, n_sm);
+    case 6: return launch_add6_t<6>(out, a, b, n_inst, st, n_sm);
+    case 7: return launch_add6_t<7>(out, a, b, n_inst, st, n_sm);
+    case 8: return launch_add6_t<8>(out, a, b, n_inst, st, n_sm);
+    case 9: return launch_add6_t<9>(out, a, b, n_inst, st, n_sm);
+    case 10: return launch_add6_t<10>(out, a, b, n_inst, st, n_sm);
+    case 11: return launch_add6_t<11>(out, a, b, n_inst, st, n_sm);
+    case 12: return launch_add6_t<12>(out, a, b, n_inst, st, n_sm);
+    case 13: return launch_add6_t<13>(out, a, b, n_inst, st, n_sm);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -263,9 +263,51 @@ bn_status run_op(int op, void* out, const void* a, const void* b, uint64_t n_ins
     case BN_OP_ADD: e = bn::launch_add(logm, o, x, y, n_inst, st, d->n_sm); break;
     case BN_OP_MUL_CLASSICAL: e = bn::launch_mul_classical(logm, o, x, y, n_inst, st, d->n_sm); break;
     case BN_OP_MUL_NTT: e = bn::launch_mul_ntt(logm, o, x, y, n_inst, d->tables[logm + 1], st, d->n_sm); break;
+    case BN_OP_ADD6: e = bn::launch_add6(logm, o, x, y, n_inst, st, d->n_sm); break;
     default: return BN_EINVAL;
   }
   return e == cudaSuccess ? BN_OK : cuda_fail(e);
+}
+
+bool is_poly(int op) { return op == BN_OP_POLY_CLASSICAL || op == BN_OP_POLY_NTT; }
+
+// workspace words of a Poly call (one slice per resident CTA of its grid)
+bn_status poly_ws_words(int op, int logm, uint64_t n_inst, const DevState* d, uint64_t* words) {
+  cudaError_t e = op == BN_OP_POLY_CLASSICAL ? bn::poly_classical_geometry(logm, n_inst, d->n_sm, words)
+                                             : bn::poly_ntt_geometry(logm, n_inst, d->n_sm, words);
+  return e == cudaSuccess ? BN_OK : cuda_fail(e);
+}
+
+bn_status launch_poly(int op, int logm, uint32_t* o, const uint32_t* x, const uint32_t* y, uint64_t n_inst,
+                      uint32_t* ws, uint64_t ws_words, cudaStream_t st, const DevState* d) {
+  cudaError_t e = op == BN_OP_POLY_CLASSICAL
+                      ? bn::launch_poly_classical(logm, o, x, y, n_inst, ws, ws_words, st, d->n_sm)
+                      : bn::launch_poly_ntt(logm, o, x, y, n_inst, d->tables[logm + 1], ws, ws_words, st, d->n_sm);
+  return e == cudaSuccess ? BN_OK : cuda_fail(e);
+}
+
+bn_status run_poly(int op, void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+                   uint32_t limb_bits, void* ws, uint64_t ws_bytes, cudaStream_t st) {
+  int logm = 0;
+  bn_status s = validate(out, a, b, n_inst, n_limbs, limb_bits, &logm);
+  if (s != BN_OK || n_inst == 0) return s;
+  DevState* d = nullptr;
+  s = current_device(&d);
+  if (s != BN_OK) return s;
+  uint64_t need = 0;
+  s = poly_ws_words(op, logm, n_inst, d, &need);
+  if (s != BN_OK) return s;
+  if (!ws || ((uintptr_t)ws & 15)) return ws ? BN_EALIGN : BN_EINVAL;
+  if (ws_bytes < need * 4) return BN_EINVAL;
+  const uint64_t bytes = n_inst * ((uint64_t)n_limbs * limb_bits / 8);
+  auto overl = [](const void* x, uint64_t xn, const void* y, uint64_t yn) {
+    const uintptr_t x0 = (uintptr_t)x, y0 = (uintptr_t)y;
+    return x0 < y0 + yn && y0 < x0 + xn;
+  };
+  if (overl(ws, need * 4, out, bytes) || overl(ws, need * 4, a, bytes) || overl(ws, need * 4, b, bytes))
+    return BN_EALIAS;
+  return launch_poly(op, logm, (uint32_t*)out, (const uint32_t*)a, (const uint32_t*)b, n_inst, (uint32_t*)ws,
+                     need, st, d);
 }
 
 }  // namespace
@@ -287,6 +329,35 @@ bn_status bn_mul_ntt(void* out, const void* a, const void* b, uint64_t n_inst, u
   return run_op(BN_OP_MUL_NTT, out, a, b, n_inst, n_limbs, limb_bits, (cudaStream_t)stream);
 }
 
+bn_status bn_add6(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits,
+                  bn_stream_t stream) {
+  return run_op(BN_OP_ADD6, out, a, b, n_inst, n_limbs, limb_bits, (cudaStream_t)stream);
+}
+
+uint64_t bn_poly_workspace_bytes(int op, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits) {
+  if (!is_poly(op)) return 0;
+  int logm = 0;
+  if (validate((void*)16, (void*)16, (void*)16, 0, n_limbs, limb_bits, &logm) != BN_OK) return 0;
+  if (n_inst == 0) return 0;
+  DevState* d = nullptr;
+  if (current_device(&d) != BN_OK) return 0;
+  uint64_t w = 0;
+  if (poly_ws_words(op, logm, n_inst, d, &w) != BN_OK) return 0;
+  return w * 4;
+}
+
+bn_status bn_poly_classical(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+                            uint32_t limb_bits, void* workspace, uint64_t workspace_bytes, bn_stream_t stream) {
+  return run_poly(BN_OP_POLY_CLASSICAL, out, a, b, n_inst, n_limbs, limb_bits, workspace, workspace_bytes,
+                  (cudaStream_t)stream);
+}
+
+bn_status bn_poly_ntt(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+                      uint32_t limb_bits, void* workspace, uint64_t workspace_bytes, bn_stream_t stream) {
+  return run_poly(BN_OP_POLY_NTT, out, a, b, n_inst, n_limbs, limb_bits, workspace, workspace_bytes,
+                  (cudaStream_t)stream);
+}
+
 bn_status bn_prepare(int device) {
   DevState* d = nullptr;
   return ensure_device(device, &d);
@@ -303,7 +374,7 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   if (!a || !b) return BN_EINVAL;
   for (int i = 0; i < n_ops; i++) {
     if (!outs[i]) return BN_EINVAL;
-    if (ops[i] < BN_OP_ADD || ops[i] > BN_OP_MUL_NTT) return BN_EINVAL;
+    if (ops[i] < BN_OP_ADD || ops[i] > BN_OP_POLY_NTT) return BN_EINVAL;
   }
   DevState* d = nullptr;
   s = current_device(&d);
@@ -314,7 +385,17 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   if (chunk < 1) chunk = 1;
   if (chunk > n_inst) chunk = n_inst;
   const size_t chunk_bytes = chunk * inst_bytes;
-  const size_t per_stream = chunk_bytes * (2 + (size_t)n_ops);
+  // Poly workspace per stream (the largest of the two methods' needs for one chunk)
+  uint64_t ws_words = 0;
+  for (int i = 0; i < n_ops; i++) {
+    if (!is_poly(ops[i])) continue;
+    uint64_t w = 0;
+    s = poly_ws_words(ops[i], logm, chunk, d, &w);
+    if (s != BN_OK) return s;
+    if (w > ws_words) ws_words = w;
+  }
+  const size_t ws_bytes = ((size_t)ws_words * 4 + 255) & ~(size_t)255;
+  const size_t per_stream = chunk_bytes * (2 + (size_t)n_ops) + ws_bytes;
   std::lock_guard<std::mutex> lk(g_mu);  // scratch is per device, one pipeline at a time
   cudaError_t e;
   if (!d->st[0]) {
@@ -347,10 +428,17 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
     if (e != cudaSuccess) return cuda_fail(e);
     for (int k = 0; k < n_ops; k++) {
       uint32_t* dout = (uint32_t*)(base + (2 + k) * chunk_bytes);
+      uint32_t* dws = (uint32_t*)(base + (2 + n_ops) * chunk_bytes);
       switch (ops[k]) {
         case BN_OP_ADD: e = bn::launch_add(logm, dout, da, db, n, st, d->n_sm); break;
         case BN_OP_MUL_CLASSICAL: e = bn::launch_mul_classical(logm, dout, da, db, n, st, d->n_sm); break;
-        default: e = bn::launch_mul_ntt(logm, dout, da, db, n, d->tables[logm + 1], st, d->n_sm); break;
+        case BN_OP_MUL_NTT: e = bn::launch_mul_ntt(logm, dout, da, db, n, d->tables[logm + 1], st, d->n_sm); break;
+        case BN_OP_ADD6: e = bn::launch_add6(logm, dout, da, db, n, st, d->n_sm); break;
+        default: {
+          s = launch_poly(ops[k], logm, dout, da, db, n, dws, ws_words, st, d);
+          if (s != BN_OK) return s;
+          e = cudaSuccess;
+        }
       }
       if (e != cudaSuccess) return cuda_fail(e);
       e = cudaMemcpyAsync((char*)outs[k] + i0 * inst_bytes, dout, bytes, cudaMemcpyDeviceToHost, st);
@@ -382,7 +470,7 @@ const char* bn_status_string(bn_status s) {
 }
 
 uint32_t bn_launches_per_call(int op, uint32_t bits) {
-  if (op < BN_OP_ADD || op > BN_OP_MUL_NTT) return 0;
+  if (op < BN_OP_ADD || op > BN_OP_POLY_NTT) return 0;
   const int lb = ilog2_exact(bits);
   if (lb < 10 || lb > 18) return 0;
   return 1;

@@ -55,6 +55,35 @@ BN_DEV void store_limbs(uint32_t* dst, const uint32_t (&r)[L]) {
     stg_stream(reinterpret_cast<uint4*>(dst) + v,
                make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
 }
+// Coherent (L2) 128-bit load / write-back store, for buffers that the same
+// kernel writes and later reads back (the fused workloads' per-CTA workspace:
+// ld.global.nc must not be used on data written during the kernel).
+template <int L>
+BN_DEV void ldcg_limbs(uint32_t (&r)[L], const uint32_t* src) {
+#pragma unroll
+  for (int v = 0; v < L / 4; v++) {
+    uint4 x = __ldcg(reinterpret_cast<const uint4*>(src) + v);
+    r[4 * v + 0] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+  }
+}
+template <int L>
+BN_DEV void stg_limbs(uint32_t* dst, const uint32_t (&r)[L]) {
+#pragma unroll
+  for (int v = 0; v < L / 4; v++)
+    reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+}
+// HBM operand (ld.global.nc, streaming) or in-kernel workspace (ld.global.cg)
+template <bool WS, int L>
+BN_DEV void load_any(uint32_t (&r)[L], const uint32_t* src) {
+  if constexpr (WS) ldcg_limbs<L>(r, src);
+  else load_limbs<L>(r, src);
+}
+template <bool WS, int L>
+BN_DEV void store_any(uint32_t* dst, const uint32_t (&r)[L]) {
+  if constexpr (WS) stg_limbs<L>(dst, r);
+  else store_limbs<L>(dst, r);
+}
+
 template <int L>
 BN_DEV void lds_limbs(uint32_t (&r)[L], const uint32_t* src) {
 #pragma unroll

@@ -55,6 +55,18 @@ cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, con
                                  uint64_t n_inst, cudaStream_t st, int n_sm);
 cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                            uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm);
+// Fused workloads: 6-Add and Poly.  The Poly kernels use
+// a caller-provided workspace of ws_words u32 words, sized by *_geometry for
+// the same (logm, n_inst, n_sm) — one slice per resident CTA.
+cudaError_t launch_add6(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                        cudaStream_t st, int n_sm);
+cudaError_t poly_classical_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words);
+cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                  uint64_t n_inst, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
+                                  int n_sm);
+cudaError_t poly_ntt_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words);
+cudaError_t launch_poly_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                            const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st, int n_sm);
 cudaError_t launch_ntt_forward_debug(int lgn, uint32_t* x, uint64_t n_inst, int prime,
                                      const NttTables& tb, cudaStream_t st);
 

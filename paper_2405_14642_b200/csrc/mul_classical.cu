@@ -120,6 +120,107 @@ BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_
   lhcs[Q + 1] = c_res;
 }
 
+// Thread roles inside a CTA (see MulCCfg): the convolution mapping
+// interleaves instances across warp lanes; the resolve mapping is
+// instance-major with G consecutive threads per instance.
+template <class C>
+struct MulCRoles {
+  int t, conv_slot, g, add_slot, chunk;
+  BN_DEV MulCRoles() {
+    t = threadIdx.x;
+    const int set = t / C::SET_T;
+    const int r = t % C::SET_T;
+    conv_slot = set * C::I + (r % C::I);
+    g = r / C::I;
+    add_slot = t / C::G;
+    chunk = t % C::G;
+  }
+};
+
+// B[-Q..-1] = 0 for every instance slot of `n_stages` stage buffers (never
+// overwritten: loads and H start at B[0]).
+template <class C>
+BN_DEV void zero_b_prefix(uint32_t* sm, int n_stages) {
+  for (int v = threadIdx.x; v < n_stages * C::IPB * C::Q; v += C::T) {
+    const int st = v / (C::IPB * C::Q), k = (v / C::Q) % C::IPB;
+    sm[st * C::STAGE_WORDS + C::IPB * C::SA + k * C::SB + (v % C::Q)] = 0u;
+  }
+}
+
+// Stage x, y of one instance group with cp.async:
+// coalesced 16-byte copies global -> shared; slots k >= n_valid are
+// zero-filled.  x, y point at the group's first instance (stride M words).
+template <class C>
+BN_DEV void stage_xy(uint32_t* As, const uint32_t* x, const uint32_t* y, uint64_t n_valid) {
+  constexpr int VPI = C::M / 4;  // uint4 per instance operand
+  uint32_t* Bs = As + C::IPB * C::SA;
+  for (int v = threadIdx.x; v < C::IPB * VPI; v += C::T) {
+    const int k = v / VPI, w = (v % VPI) * 4;
+    const bool ok = (uint64_t)k < n_valid;
+    const uint64_t off = ok ? (uint64_t)k * C::M + w : 0;
+    cp_async16(As + k * C::SA + w, x + off, ok);
+    cp_async16(Bs + k * C::SB + C::Q + w, y + off, ok);
+  }
+}
+
+// Convolution (Fig. 7) of the staged group and the L/H publish (reading R8),
+// L over the A area, H over the B area.  Ends with a CTA barrier.
+template <class C>
+BN_DEV void conv_publish(uint32_t* As, const MulCRoles<C>& ro) {
+  constexpr int M = C::M, Q = C::Q;
+  uint32_t* Bs = As + C::IPB * C::SA;
+  // ---- convolution: low chunk j0 = g and mirror chunk j0' = M/Q - 1 - g
+  uint32_t lh0[Q + 2], lh1[Q + 2];
+  {
+    const uint32_t* Ai = As + ro.conv_slot * C::SA;
+    const uint32_t* Bi = Bs + ro.conv_slot * C::SB + Q;
+    conv_chunk<Q>(Ai, Bi, ro.g, lh0);
+    conv_chunk<Q>(Ai, Bi, M / Q - 1 - ro.g, lh1);
+  }
+  __syncthreads();
+  // ---- publish (reading R8): L[k1+q] = low_q; H[k1+Q] = high; H[k1+Q+1] = carry;
+  // H[k1+Q+2 .. k1+2Q) = 0; the top chunk zeroes H[0..Q) instead.
+  {
+    uint32_t* L = As + ro.conv_slot * C::SA;
+    uint32_t* H = Bs + ro.conv_slot * C::SB + Q;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t* lh = h == 0 ? lh0 : lh1;
+      const int j0 = h == 0 ? ro.g : M / Q - 1 - ro.g;
+      const int k1 = Q * j0;
+      uint32_t lows[Q], hs[Q];
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        lows[q] = lh[q];
+        hs[q] = q == 0 ? lh[Q] : (q == 1 ? lh[Q + 1] : 0u);
+      }
+      sts_limbs<Q>(L + k1, lows);
+      if (k1 + Q < M) {
+        sts_limbs<Q>(H + k1 + Q, hs);
+      } else {
+        uint32_t z[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) z[q] = 0;
+        sts_limbs<Q>(H, z);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Resolve R = L + H into this thread's 2Q limbs
+// (resolve mapping: limbs [2Q chunk, 2Q chunk + 2Q) of instance add_slot).
+template <class C>
+BN_DEV void resolve_lh(const uint32_t* As, const MulCRoles<C>& ro, bool valid, uint32_t* agg,
+                       uint32_t (&res)[2 * C::Q]) {
+  constexpr int L2 = 2 * C::Q;
+  const uint32_t* Bs = As + C::IPB * C::SA;
+  uint32_t x[L2], y[L2];
+  lds_limbs<L2>(x, As + ro.add_slot * C::SA + L2 * ro.chunk);
+  lds_limbs<L2>(y, Bs + ro.add_slot * C::SB + C::Q + L2 * ro.chunk);
+  add_regs<L2, C::G>(x, y, res, valid, agg);
+}
+
 template <int LOGM, int Q>
 __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
     mul_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
@@ -127,39 +228,14 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* agg = sm + 2 * C::STAGE_WORDS;  // T/32
-
-  const int t = threadIdx.x;
-  // convolution mapping: lane = inst_lo + I * g_lo (instance-fastest)
-  const int set = t / C::SET_T;
-  const int r = t % C::SET_T;
-  const int conv_slot = set * C::I + (r % C::I);
-  const int g = r / C::I;
-  // resolve/store mapping: instance-major, G consecutive threads per instance
-  const int add_slot = t / C::G;
-  const int chunk = t % C::G;
-
-  // B[-Q..-1] = 0 in both stages (never overwritten: loads and H start at B[0])
-  for (int v = t; v < 2 * C::IPB * Q; v += C::T) {
-    const int st = v / (C::IPB * Q), k = (v / Q) % C::IPB;
-    sm[st * C::STAGE_WORDS + C::IPB * C::SA + k * C::SB + (v % Q)] = 0u;
-  }
-  // stage A, B of a group with cp.async: coalesced 16-byte
-  // copies global -> shared, zero-filled past the last instance
-  constexpr int VPI = M / 4;  // uint4 per instance operand
-  auto issue = [&](uint64_t grp, int st) {
-    uint32_t* As = sm + st * C::STAGE_WORDS;
-    uint32_t* Bs = As + C::IPB * C::SA;
-    const uint64_t i0 = grp * C::IPB;
-    for (int v = t; v < C::IPB * VPI; v += C::T) {
-      const int k = v / VPI, w = (v % VPI) * 4;
-      const bool ok = i0 + k < n_inst;
-      const uint64_t off = ok ? (i0 + k) * M + w : 0;
-      cp_async16(As + k * C::SA + w, a + off, ok);
-      cp_async16(Bs + k * C::SB + Q + w, b + off, ok);
-    }
-  };
+  const MulCRoles<C> ro;
+  zero_b_prefix<C>(sm, 2);
 
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  auto issue = [&](uint64_t grp, int st) {
+    const uint64_t i0 = grp * C::IPB;
+    stage_xy<C>(sm + st * C::STAGE_WORDS, a + i0 * M, b + i0 * M, n_inst - i0);
+  };
   uint64_t grp = blockIdx.x;
   if (grp < n_groups) issue(grp, 0);
   cp_async_commit();
@@ -170,62 +246,81 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
     cp_async_wait<1>();
     __syncthreads();
     uint32_t* As = sm + st * C::STAGE_WORDS;
-    uint32_t* Bs = As + C::IPB * C::SA;
-    const uint64_t inst0 = grp * C::IPB;
-
-    // ---- convolution: low chunk j0 = g and mirror chunk j0' = M/Q - 1 - g
-    uint32_t lh0[Q + 2], lh1[Q + 2];
-    {
-      const uint32_t* Ai = As + conv_slot * C::SA;
-      const uint32_t* Bi = Bs + conv_slot * C::SB + Q;
-      conv_chunk<Q>(Ai, Bi, g, lh0);
-      conv_chunk<Q>(Ai, Bi, M / Q - 1 - g, lh1);
-    }
-    __syncthreads();
-
-    // ---- publish (reading R8): L[k1+q] = low_q; H[k1+Q] = high; H[k1+Q+1] = carry;
-    // H[k1+Q+2 .. k1+2Q) = 0; the top chunk zeroes H[0..Q) instead.
-    {
-      uint32_t* L = As + conv_slot * C::SA;
-      uint32_t* H = Bs + conv_slot * C::SB + Q;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const uint32_t* lh = h == 0 ? lh0 : lh1;
-        const int j0 = h == 0 ? g : M / Q - 1 - g;
-        const int k1 = Q * j0;
-        uint32_t lows[Q], hs[Q];
-#pragma unroll
-        for (int q = 0; q < Q; q++) {
-          lows[q] = lh[q];
-          hs[q] = q == 0 ? lh[Q] : (q == 1 ? lh[Q + 1] : 0u);
-        }
-        sts_limbs<Q>(L + k1, lows);
-        if (k1 + Q < M) {
-          sts_limbs<Q>(H + k1 + Q, hs);
-        } else {
-          uint32_t z[Q];
-#pragma unroll
-          for (int q = 0; q < Q; q++) z[q] = 0;
-          sts_limbs<Q>(H, z);
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- resolve R = L + H and store
-    {
-      constexpr int L2 = 2 * Q;
-      const uint64_t inst = inst0 + add_slot;
-      const bool valid = inst < n_inst;
-      uint32_t x[L2], y[L2], res[L2];
-      lds_limbs<L2>(x, As + add_slot * C::SA + L2 * chunk);
-      lds_limbs<L2>(y, Bs + add_slot * C::SB + Q + L2 * chunk);
-      add_regs<L2, C::G>(x, y, res, valid, agg);
-      if (valid) store_limbs<L2>(out + inst * M + L2 * chunk, res);
-    }
+    const uint64_t inst = grp * C::IPB + ro.add_slot;
+    const bool valid = inst < n_inst;
+    conv_publish<C>(As, ro);
+    uint32_t res[2 * Q];
+    resolve_lh<C>(As, ro, valid, agg, res);
+    if (valid) store_limbs<2 * Q>(out + inst * M + 2 * Q * ro.chunk, res);
     __syncthreads();  // this stage is refilled two groups from now
   }
   cp_async_wait<0>();
+}
+
+// Poly (Table 2 caption): (a*a + b) * (b*b + b) + a*b
+// mod 2^bits — four classical multiplications and three additions in ONE
+// kernel (block-level fusion).  Every phase is one multiplication of the
+// kernel above with the addition fused into its epilogue (a second scan-add
+// on the resolved product); the three intermediates t1 = a^2 + b,
+// t2 = b^2 + b, t3 = a b go to this CTA's private slice of the caller's
+// workspace (L2-resident: it is rewritten group after group by the same
+// CTA) and come back as the operands of the last phase.
+//   phase 1: t1 = a*a + b    phase 2: t2 = b*b + b
+//   phase 3: t3 = a*b        phase 4: out = t1*t2 + t3
+template <class C, bool AWS, bool OWS>
+BN_DEV void classical_phase(uint32_t* As, uint32_t* agg, const MulCRoles<C>& ro, const uint32_t* x,
+                            const uint32_t* y, const uint32_t* addend, uint32_t* dst, uint64_t n_valid) {
+  constexpr int Q = C::Q, M = C::M;
+  stage_xy<C>(As, x, y, n_valid);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  conv_publish<C>(As, ro);
+  const bool valid = (uint64_t)ro.add_slot < n_valid;
+  const uint64_t off = (uint64_t)ro.add_slot * M + 2 * Q * ro.chunk;
+  uint32_t res[2 * Q];
+  resolve_lh<C>(As, ro, valid, agg, res);
+  if (addend) {
+    uint32_t ad[2 * Q], r2[2 * Q];
+    if (valid) load_any<AWS, 2 * Q>(ad, addend + off);
+    else {
+#pragma unroll
+      for (int i = 0; i < 2 * Q; i++) ad[i] = 0;
+    }
+    if constexpr (C::G > 32) __syncthreads();  // agg reuse
+    add_regs<2 * Q, C::G>(res, ad, r2, valid, agg);
+    if (valid) store_any<OWS, 2 * Q>(dst + off, r2);
+  } else {
+    if (valid) store_any<OWS, 2 * Q>(dst + off, res);
+  }
+  __syncthreads();  // dst visible to the next phase; As / agg free
+}
+
+template <int LOGM, int Q>
+__global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
+    poly_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                          uint32_t* ws) {
+  using C = MulCCfg<LOGM, Q>;
+  constexpr int M = C::M;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* agg = sm + C::STAGE_WORDS;  // T/32
+  const MulCRoles<C> ro;
+  zero_b_prefix<C>(sm, 1);
+  // this CTA's workspace slice: t1 | t2 | t3, each IPB * M words
+  uint32_t* t1 = ws + (uint64_t)blockIdx.x * 3 * C::IPB * M;
+  uint32_t* t2 = t1 + C::IPB * M;
+  uint32_t* t3 = t2 + C::IPB * M;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t i0 = grp * C::IPB;
+    const uint64_t nv = n_inst - i0 < (uint64_t)C::IPB ? n_inst - i0 : (uint64_t)C::IPB;
+    const uint32_t* ag = a + i0 * M;
+    const uint32_t* bg = b + i0 * M;
+    classical_phase<C, false, true>(sm, agg, ro, ag, ag, bg, t1, nv);
+    classical_phase<C, false, true>(sm, agg, ro, bg, bg, bg, t2, nv);
+    classical_phase<C, false, true>(sm, agg, ro, ag, bg, nullptr, t3, nv);
+    classical_phase<C, true, false>(sm, agg, ro, t1, t2, t3, out + i0 * M, nv);
+  }
 }
 
 template <int LOGM>
@@ -246,6 +341,66 @@ static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_
   const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
   mul_classical_kernel<LOGM, Q><<<grid, C::T, smem, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
+}
+
+// Poly: one resident wave of persistent CTAs (each owns one workspace slice).
+template <int LOGM>
+static cudaError_t poly_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64_t* ws_words) {
+  constexpr int Q = 4;
+  using C = MulCCfg<LOGM, Q>;
+  constexpr size_t smem = (C::STAGE_WORDS + C::T / 32) * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(poly_classical_kernel<LOGM, Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, poly_classical_kernel<LOGM, Q>, C::T, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;
+  *grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
+  *ws_words = (uint64_t)*grid * 3 * C::IPB * C::M;
+  return cudaSuccess;
+}
+
+template <int LOGM>
+static cudaError_t launch_polyc_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                  uint32_t* ws, uint64_t ws_words, cudaStream_t st, int n_sm) {
+  constexpr int Q = 4;
+  using C = MulCCfg<LOGM, Q>;
+  unsigned grid = 0;
+  uint64_t need = 0;
+  cudaError_t e = poly_geom_t<LOGM>(n_inst, n_sm, &grid, &need);
+  if (e != cudaSuccess) return e;
+  if (ws_words < need) return cudaErrorInvalidValue;
+  constexpr size_t smem = (C::STAGE_WORDS + C::T / 32) * sizeof(uint32_t);
+  poly_classical_kernel<LOGM, Q><<<grid, C::T, smem, st>>>(out, a, b, n_inst, ws);
+  return cudaGetLastError();
+}
+
+#define BN_LOGM_SWITCH(F, ...)                      \
+  switch (logm) {                                   \
+    case 5: return F<5>(__VA_ARGS__);               \
+    case 6: return F<6>(__VA_ARGS__);               \
+    case 7: return F<7>(__VA_ARGS__);               \
+    case 8: return F<8>(__VA_ARGS__);               \
+    case 9: return F<9>(__VA_ARGS__);               \
+    case 10: return F<10>(__VA_ARGS__);             \
+    case 11: return F<11>(__VA_ARGS__);             \
+    case 12: return F<12>(__VA_ARGS__);             \
+    case 13: return F<13>(__VA_ARGS__);             \
+    default: return cudaErrorInvalidValue;          \
+  }
+
+cudaError_t poly_classical_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words) {
+  unsigned grid = 0;
+  BN_LOGM_SWITCH(poly_geom_t, n_inst, n_sm, &grid, ws_words)
+}
+
+cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                  uint64_t n_inst, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
+                                  int n_sm) {
+  BN_LOGM_SWITCH(launch_polyc_t, out, a, b, n_inst, ws, ws_words, st, n_sm)
 }
 
 cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,

@@ -272,16 +272,19 @@ BN_DEV void add3(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t c0, uint32_t
       : "r"(c0), "r"(c1), "r"(c2));
 }
 
-// ------------------------------------------------------------ the kernel
-template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
-    mul_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
-                   const uint2* __restrict__ tw) {
+// ------------------------------------------------------------ one product
+// out = x * y (+ addend) mod 2^bits for this slot's instance: per prime
+// N-1..N-4, then CRT / publish (N-5, N-6), resolve (N-7) and, when ADD, a
+// second scan-add of the addend fused into the epilogue (the Poly workload).
+// SQ: x == y, so one forward transform serves both operands (Â * Â).
+// XWS / AWS / OWS: operand / addend / destination live in the in-kernel
+// workspace (coherent ld.global.cg, write-back stores) instead of HBM
+// (ld.global.nc, streaming stores).  Ends with a CTA barrier.
+template <int LOGN, bool SQ, bool ADD, bool XWS, bool AWS, bool OWS>
+BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const uint32_t* yi,
+                        const uint32_t* addi, uint32_t* dsti, bool valid, const uint2* __restrict__ tw) {
   using C = NttCfg<LOGN>;
   constexpr int N = C::N, M = C::M, TPI = C::TPI;
-  extern __shared__ __align__(16) uint32_t sm[];
-  const int slot = threadIdx.x / TPI;
-  const int t = threadIdx.x % TPI;
   // this slot's own (padded) exchange region, reused for L | H after the
   // transforms: it must not reach into another slot's region, because slots
   // in different warps only synchronise at CTA barriers
@@ -291,102 +294,168 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
   constexpr int RS = 3 * M + (C::TPI < 32 ? 16 : 0);
   uint32_t* Res = sm + 2 * C::XW + slot * RS;
   uint32_t* agg = sm + 2 * C::XW + C::IPB * RS;
+  constexpr int NV = SQ ? 1 : 2;
 
+#pragma unroll 1
+  for (int j = 0; j < kNumPrimes; j++) {
+    const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+    const uint2* twf = tw + (2 * j + 0) * (N - 1);
+    const uint2* twi = tw + (2 * j + 1) * (N - 1);
+    uint32_t xab[NV][16];
+    // N-1: reduce the limbs mod p into pass-0 layout (index t + e N/16),
+    // upper half is the zero padding (reading R11)
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const uint32_t* px = xi + t + e * (N / 16);
+      const uint32_t va = valid ? (XWS ? __ldcg(px) : __ldg(px)) : 0u;
+      // a_i < 2^32 < 6p: two conditional subtractions of 2p -> [0, 2p)
+      xab[0][e] = red2(red2(va, p2), p2);
+      if constexpr (!SQ) {
+        const uint32_t* py = yi + t + e * (N / 16);
+        const uint32_t vb = valid ? (XWS ? __ldcg(py) : __ldg(py)) : 0u;
+        xab[NV - 1][e] = red2(red2(vb, p2), p2);
+      }
+    }
+#pragma unroll
+    for (int e = 8; e < 16; e++) {
+#pragma unroll
+      for (int v = 0; v < NV; v++) xab[v][e] = 0u;
+    }
+    // N-2: forward transforms of x and y together (one when squaring)
+    fwd_all<LOGN, true, NV>(xab, sm, slot * N, t, twf, p, p2);
+    // N-3: pointwise product (same register layout for both transforms)
+    uint32_t x[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[NV - 1][e], p, pinv);
+    // N-4: inverse transform -> pass-0 layout, natural order
+    inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
+    // keep coefficients 0..M-1 (truncated product): e < 8
+#pragma unroll
+    for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
+  }
+  bar<TPI>();
+
+  // N-5 / N-6: Garner CRT of 8 consecutive coefficients, aggregate, publish
+  {
+    const CrtConst& k = c_crt[LOGN];
+    const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+    uint32_t y0[8], y1[8], y2[8];
+    lds_limbs<8>(y0, Res + 0 * M + 8 * t);
+    lds_limbs<8>(y1, Res + 1 * M + 8 * t);
+    lds_limbs<8>(y2, Res + 2 * M + 8 * t);
+    uint32_t lows[8], hs[8];
+    uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+      const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+      const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+      const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+      const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+      const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+      const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+      const uint32_t d = red2(b2v + c2v, 2 * p2);
+      const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+      // c = r0 + p0 t1 + p0 p1 t2  (< 2^90)
+      const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+      const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+      const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
+      add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
+      lows[q] = a0;
+      a0 = a1;
+      a1 = a2;
+      a2 = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+    // X is dead (last exchange read it before inv_pass<0>, followed by bar)
+    uint32_t* L = X;
+    uint32_t* H = X + M;
+    sts_limbs<8>(L + 8 * t, lows);
+    if (8 * t + 8 < M) {
+      sts_limbs<8>(H + 8 * t + 8, hs);
+    } else {
+      uint32_t z[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) z[q] = 0;
+      sts_limbs<8>(H, z);
+    }
+  }
+  bar<TPI>();
+  // N-7: R = L + H (+ addend), store
+  {
+    uint32_t xl[8], yh[8], r[8];
+    lds_limbs<8>(xl, X + 8 * t);
+    lds_limbs<8>(yh, X + M + 8 * t);
+    add_regs<8, TPI>(xl, yh, r, valid, agg);
+    if constexpr (ADD) {
+      uint32_t ad[8], r2[8];
+      if (valid) load_any<AWS, 8>(ad, addi + 8 * t);
+      else {
+#pragma unroll
+        for (int q = 0; q < 8; q++) ad[q] = 0;
+      }
+      if constexpr (TPI > 32) __syncthreads();  // agg reuse
+      add_regs<8, TPI>(r, ad, r2, valid, agg);
+      if (valid) store_any<OWS, 8>(dsti + 8 * t, r2);
+    } else {
+      if (valid) store_any<OWS, 8>(dsti + 8 * t, r);
+    }
+  }
+  __syncthreads();  // X / Res / agg reused next; dst visible to the CTA
+}
+
+// ------------------------------------------------------------ the kernels
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
+    mul_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                   const uint2* __restrict__ tw) {
+  using C = NttCfg<LOGN>;
+  constexpr int M = C::M;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int slot = threadIdx.x / C::TPI;
+  const int t = threadIdx.x % C::TPI;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
     const uint64_t inst = grp * C::IPB + slot;
     const bool valid = inst < n_inst;
-    const uint32_t* ai = a + (valid ? inst : 0) * M;
-    const uint32_t* bi = b + (valid ? inst : 0) * M;
+    const uint64_t io = (valid ? inst : 0) * M;
+    ntt_product<LOGN, false, false, false, false, false>(sm, slot, t, a + io, b + io, nullptr, out + io,
+                                                         valid, tw);
+  }
+}
 
-#pragma unroll 1
-    for (int j = 0; j < kNumPrimes; j++) {
-      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
-      const uint2* twf = tw + (2 * j + 0) * (N - 1);
-      const uint2* twi = tw + (2 * j + 1) * (N - 1);
-      uint32_t xab[2][16];
-      // N-1: reduce the limbs mod p into pass-0 layout (index t + e N/16),
-      // upper half is the zero padding (reading R11)
-#pragma unroll
-      for (int e = 0; e < 8; e++) {
-        const uint32_t va = valid ? __ldg(ai + t + e * (N / 16)) : 0u;
-        const uint32_t vb = valid ? __ldg(bi + t + e * (N / 16)) : 0u;
-        // a_i < 2^32 < 6p: two conditional subtractions of 2p -> [0, 2p)
-        xab[0][e] = red2(red2(va, p2), p2);
-        xab[1][e] = red2(red2(vb, p2), p2);
-      }
-#pragma unroll
-      for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
-      // N-2: forward transforms of A and B together
-      fwd_all<LOGN, true, 2>(xab, sm, slot * N, t, twf, p, p2);
-      // N-3: pointwise product (same register layout for A-hat and B-hat)
-      uint32_t x[16];
-#pragma unroll
-      for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[1][e], p, pinv);
-      // N-4: inverse transform -> pass-0 layout, natural order
-      inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
-      // keep coefficients 0..M-1 (truncated product): e < 8
-#pragma unroll
-      for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
-    }
-    bar<TPI>();
-
-    // N-5 / N-6: Garner CRT of 8 consecutive coefficients, aggregate, publish
-    {
-      const CrtConst& k = c_crt[LOGN];
-      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-      uint32_t y0[8], y1[8], y2[8];
-      lds_limbs<8>(y0, Res + 0 * M + 8 * t);
-      lds_limbs<8>(y1, Res + 1 * M + 8 * t);
-      lds_limbs<8>(y2, Res + 2 * M + 8 * t);
-      uint32_t lows[8], hs[8];
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-        const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-        const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-        const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-        const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-        const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-        const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-        const uint32_t d = red2(b2v + c2v, 2 * p2);
-        const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-        // c = r0 + p0 t1 + p0 p1 t2  (< 2^90)
-        const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-        const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-        const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
-        add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
-        lows[q] = a0;
-        a0 = a1;
-        a1 = a2;
-        a2 = 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
-      // X is dead (last exchange read it before inv_pass<0>, followed by bar)
-      uint32_t* L = X;
-      uint32_t* H = X + M;
-      sts_limbs<8>(L + 8 * t, lows);
-      if (8 * t + 8 < M) {
-        sts_limbs<8>(H + 8 * t + 8, hs);
-      } else {
-        uint32_t z[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) z[q] = 0;
-        sts_limbs<8>(H, z);
-      }
-    }
-    bar<TPI>();
-    // N-7: R = L + H, store
-    {
-      uint32_t xl[8], yh[8], r[8];
-      lds_limbs<8>(xl, X + 8 * t);
-      lds_limbs<8>(yh, X + M + 8 * t);
-      add_regs<8, TPI>(xl, yh, r, valid, agg);
-      if (valid) store_limbs<8>(out + inst * M + 8 * t, r);
-    }
-    __syncthreads();  // X / Res / agg reused by the next group
+// Poly (Table 2 caption): (a*a + b) * (b*b + b) + a*b
+// mod 2^bits in ONE kernel — four NTT products with the three additions
+// fused into their epilogues (block-level fusion).  a^2 and b^2 each need a
+// single forward transform (SQ), so a group costs 10 transforms per prime
+// instead of 12.  The intermediates t1 = a^2 + b, t2 = b^2 + b, t3 = a b go
+// to this CTA's private workspace slice (L2-resident, rewritten by the same
+// CTA group after group) and are read back coherently by the last product.
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
+    poly_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                    const uint2* __restrict__ tw, uint32_t* ws) {
+  using C = NttCfg<LOGN>;
+  constexpr int M = C::M;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int slot = threadIdx.x / C::TPI;
+  const int t = threadIdx.x % C::TPI;
+  uint32_t* t1 = ws + ((uint64_t)blockIdx.x * C::IPB + slot) * 3 * M;
+  uint32_t* t2 = t1 + M;
+  uint32_t* t3 = t2 + M;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t inst = grp * C::IPB + slot;
+    const bool valid = inst < n_inst;
+    const uint64_t io = (valid ? inst : 0) * M;
+    const uint32_t* ai = a + io;
+    const uint32_t* bi = b + io;
+    //                 SQ     ADD    XWS    AWS    OWS
+    ntt_product<LOGN, true, true, false, false, true>(sm, slot, t, ai, ai, bi, t1, valid, tw);
+    ntt_product<LOGN, true, true, false, false, true>(sm, slot, t, bi, bi, bi, t2, valid, tw);
+    ntt_product<LOGN, false, false, false, false, true>(sm, slot, t, ai, bi, nullptr, t3, valid, tw);
+    ntt_product<LOGN, false, true, true, true, false>(sm, slot, t, t1, t2, t3, out + io, valid, tw);
   }
 }
 
@@ -439,6 +508,39 @@ static cudaError_t launch_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t
 }
 
 template <int LOGN>
+static cudaError_t poly_ntt_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64_t* ws_words) {
+  using C = NttCfg<LOGN>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(poly_ntt_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, poly_ntt_kernel<LOGN>, C::T, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;  // one resident wave: one workspace slice each
+  *grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
+  *ws_words = (uint64_t)*grid * C::IPB * 3 * C::M;
+  return cudaSuccess;
+}
+
+template <int LOGN>
+static cudaError_t launch_poly_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                     const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
+                                     int n_sm) {
+  using C = NttCfg<LOGN>;
+  unsigned grid = 0;
+  uint64_t need = 0;
+  cudaError_t e = poly_ntt_geom_t<LOGN>(n_inst, n_sm, &grid, &need);
+  if (e != cudaSuccess) return e;
+  if (ws_words < need) return cudaErrorInvalidValue;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  poly_ntt_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw, ws);
+  return cudaGetLastError();
+}
+
+template <int LOGN>
 static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const NttTables& tb,
                                 cudaStream_t st) {
   using C = NttCfg<LOGN>;
@@ -482,6 +584,30 @@ cudaError_t launch_ntt_forward_debug(int lgn, uint32_t* x, uint64_t n_inst, int 
     case 14: return launch_dbg_t<14>(x, n_inst, prime, tb, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+#define BN_LOGN_SWITCH(F, ...)            \
+  switch (logm + 1) {                     \
+    case 6: return F<6>(__VA_ARGS__);     \
+    case 7: return F<7>(__VA_ARGS__);     \
+    case 8: return F<8>(__VA_ARGS__);     \
+    case 9: return F<9>(__VA_ARGS__);     \
+    case 10: return F<10>(__VA_ARGS__);   \
+    case 11: return F<11>(__VA_ARGS__);   \
+    case 12: return F<12>(__VA_ARGS__);   \
+    case 13: return F<13>(__VA_ARGS__);   \
+    case 14: return F<14>(__VA_ARGS__);   \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t poly_ntt_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words) {
+  unsigned grid = 0;
+  BN_LOGN_SWITCH(poly_ntt_geom_t, n_inst, n_sm, &grid, ws_words)
+}
+
+cudaError_t launch_poly_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                            const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st, int n_sm) {
+  BN_LOGN_SWITCH(launch_poly_ntt_t, out, a, b, n_inst, tb, ws, ws_words, st, n_sm)
 }
 
 }  // namespace bn

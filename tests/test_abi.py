@@ -65,7 +65,7 @@ def _call(lib, name, out, a, b, n, limbs, bits):
     return getattr(lib, name)(vp(out), vp(a), vp(b), n, limbs, bits, None)
 
 
-OPS = ["bn_add", "bn_mul_classical", "bn_mul_ntt"]
+OPS = ["bn_add", "bn_mul_classical", "bn_mul_ntt", "bn_add6"]
 
 
 @pytest.mark.parametrize("op", OPS)
@@ -94,7 +94,7 @@ def test_u64_size_rules(lib):
 def test_introspection(lib):
     assert lib.bn_max_bits() == 262144 and lib.bn_min_bits() == 1024
     assert lib.bn_status_string(3).startswith(b"BN_EALIGN")
-    for op in range(3):
+    for op in range(6):
         assert lib.bn_launches_per_call(op, 4096) == 1
         assert lib.bn_launches_per_call(op, 3000) == 0
     arr = (ctypes.c_uint32 * 3)()
@@ -121,3 +121,22 @@ def test_ntt_primes_are_prime_with_roots(lib):
     ps = bn.ntt_primes()
     assert all(is_prime(p) for p in ps)
     assert ps[0] * ps[1] * ps[2] > 8192 * (2**32 - 1) ** 2
+
+
+@pytest.mark.parametrize("op", ["bn_poly_classical", "bn_poly_ntt"])
+def test_poly_validation_before_launch(lib, op):
+    """The fused Poly entry points validate like bn_add before touching a
+    device (the workspace is checked after sizing, on the device)."""
+    A, B, O, W = 0x10000, 0x200000, 0x4000000, 0x8000000
+    f = getattr(lib, op)
+    call = lambda o, a, b, n, limbs, bits: f(vp(o), vp(a), vp(b), n, limbs, bits, vp(W), 1 << 20, None)
+    assert call(O, A, B, 4, 32, 7) == 1
+    assert call(O, A, B, 4, 48, 32) == 2
+    assert call(O, A, B, 4, 16384, 32) == 2
+    assert call(O, A, B, 0, 32, 32) == 0
+    assert call(O, A + 4, B, 4, 32, 32) == 3
+    assert call(A + 16, A, B, 4, 32, 32) == 4
+    # invalid arguments -> 0 workspace bytes (no device needed)
+    assert lib.bn_poly_workspace_bytes(4, 10, 48, 32) == 0
+    assert lib.bn_poly_workspace_bytes(0, 10, 32, 32) == 0
+    assert lib.bn_poly_workspace_bytes(5, 0, 32, 32) == 0

@@ -246,3 +246,123 @@ def test_run_host_pipeline(bits):
     idx = [0, n // 3, n - 1]
     an, bnp = inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx])
     assert np.array_equal(inputs.to_numpy_u32(outs[1][idx]), O.mul(an, bnp))
+
+
+# ------------------------------------- fused workloads: 6-Add, Poly (§8(f) #1)
+
+FUSED = {"add6": (bn.add6, O.add6), "poly_classical": (bn.poly_classical, O.poly),
+         "poly_ntt": (bn.poly_ntt, O.poly)}
+
+
+@pytest.mark.parametrize("cls", ["U", "ONES", "RIPPLE", "RUNS", "MIX"])
+@pytest.mark.parametrize("bits", SIZES)
+def test_parity_fused(bits, cls):
+    """6-Add and Poly (classical and NTT) vs the oracle's compositions,
+    bit-exact, several CTAs + a ragged tail at every size."""
+    m = bits // 32
+    n = N_INST[bits]
+    a, b = inputs.make_operands(n, m, seed=3 * bits + len(cls), cls=cls)
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    da, db = a.to(DEV), b.to(DEV)
+    want6 = O.add6(an, bnp, nthreads=8)
+    wantp = O.poly(an, bnp, nthreads=8)
+    for name, (f, _) in FUSED.items():
+        got = inputs.to_numpy_u32(f(da, db))
+        bad = _first_bad(got, want6 if name == "add6" else wantp)
+        assert bad is None, "%s %d bits %s: %s" % (name, bits, cls, bad)
+
+
+@pytest.mark.parametrize("cap", [1, 5])
+@pytest.mark.parametrize("bits", [1024, 8192, 131072])
+def test_fused_grid_cap_and_workspace_reuse(bits, cap):
+    """Persistent CTAs that each run many groups reuse their workspace slice
+    group after group; results must not change (R20)."""
+    m = bits // 32
+    n = 203 if bits <= 8192 else 7
+    a, b = inputs.make_operands(n, m, seed=cap + 40, cls="MIX")
+    wantp = O.poly(inputs.to_numpy_u32(a), inputs.to_numpy_u32(b), nthreads=8)
+    want6 = O.add6(inputs.to_numpy_u32(a), inputs.to_numpy_u32(b))
+    da, db = a.to(DEV), b.to(DEV)
+    bn.debug_set_grid_cap(cap)
+    try:
+        got = {k: inputs.to_numpy_u32(f(da, db)) for k, (f, _) in FUSED.items()}
+    finally:
+        bn.debug_set_grid_cap(0)
+    for k, g in got.items():
+        bad = _first_bad(g, want6 if k == "add6" else wantp)
+        assert bad is None, "%s cap=%d: %s" % (k, cap, bad)
+
+
+def test_fused_u64_in_place_and_workspace_errors():
+    m = 64
+    a, b = inputs.make_operands(33, m, seed=12, cls="U")
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    da, db = a.to(DEV), b.to(DEV)
+    wantp = O.poly(an, bnp)
+    for f in (bn.poly_classical, bn.poly_ntt):
+        got = f(da.view(torch.int64), db.view(torch.int64)).view(torch.int32)
+        assert np.array_equal(inputs.to_numpy_u32(got), wantp)
+        x = da.clone()
+        f(x, db, out=x)
+        assert np.array_equal(inputs.to_numpy_u32(x), wantp)
+    x = db.clone()
+    bn.add6(da, x, out=x)
+    assert np.array_equal(inputs.to_numpy_u32(x), O.add6(an, bnp))
+    for op, f in (("poly_classical", bn.poly_classical), ("poly_ntt", bn.poly_ntt)):
+        need = bn.poly_workspace_bytes(op, 33, m)
+        assert 0 < need <= 3 * 33 * m * 4 * 2
+        ws = torch.empty(need - 16, dtype=torch.uint8, device=DEV)
+        with pytest.raises(bn.BnError):
+            f(da, db, workspace=ws)
+        ws = torch.empty(need, dtype=torch.uint8, device=DEV)
+        assert np.array_equal(inputs.to_numpy_u32(f(da, db, workspace=ws)), wantp)
+
+
+def test_fused_full_size_4096():
+    """The fused workloads at the bench size (4096 bits, 2^20 instances):
+    poly_classical == poly_ntt over the whole batch, 256 sampled instances
+    vs the oracle, and 6-Add == 4a + 3b through the single-op kernels."""
+    m, n = 128, 1 << 20
+    a, b = inputs.make_operands(n, m, seed=5, cls="U", device=DEV)
+    pc, pn = bn.poly_classical(a, b), bn.poly_ntt(a, b)
+    assert torch.equal(pc, pn)
+    s6 = bn.add6(a, b)
+    a2 = bn.add(a, a)
+    a4 = bn.add(a2, a2)
+    b3 = bn.add(bn.add(b, b), b)
+    assert torch.equal(s6, bn.add(a4, b3))
+    g = torch.Generator().manual_seed(1)
+    idx = torch.cat([torch.tensor([0, n - 1]), torch.randint(0, n, (254,), generator=g)]).to(DEV)
+    an, bnp = inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx])
+    assert np.array_equal(inputs.to_numpy_u32(pn[idx]), O.poly(an, bnp, nthreads=8))
+    assert np.array_equal(inputs.to_numpy_u32(s6[idx]), O.add6(an, bnp))
+
+
+@pytest.mark.parametrize("bits", [32768, 262144])
+def test_fused_closed_forms_full_batch(bits):
+    """Worst-case all-ones at the paper batch: Poly(-1, -1) = 1, 6-Add = -7."""
+    m = bits // 32
+    n = (1 << 32) // bits
+    ones, _ = inputs.make_operands(n, m, seed=1, cls="ONES", device=DEV)
+    one = torch.zeros((m,), dtype=torch.int32, device=DEV)
+    one[0] = 1
+    assert torch.equal(bn.poly_ntt(ones, ones), one.expand(n, m))
+    minus7 = torch.full((m,), -1, dtype=torch.int32, device=DEV)
+    minus7[0] = -7
+    assert torch.equal(bn.add6(ones, ones), minus7.expand(n, m))
+
+
+@pytest.mark.parametrize("bits", [1024, 32768])
+def test_run_host_fused(bits):
+    m = bits // 32
+    n = max(3, (1 << 26) // bits)
+    a, b = inputs.make_operands(n, m, seed=8, cls="MIX")
+    a, b = a.pin_memory(), b.pin_memory()
+    outs = bn.run_host(["add6", "poly_classical", "poly_ntt"], a, b)
+    da, db = a.to(DEV), b.to(DEV)
+    assert torch.equal(outs[0], bn.add6(da, db).cpu())
+    wp = bn.poly_ntt(da, db).cpu()
+    assert torch.equal(outs[1], wp) and torch.equal(outs[2], wp)
+    idx = [0, n // 2, n - 1]
+    assert np.array_equal(inputs.to_numpy_u32(outs[2][idx]),
+                          O.poly(inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx])))

@@ -178,3 +178,52 @@ def test_in_place_batch_and_empty():
     assert O.add(a, a).shape == (0, 8)
     with pytest.raises(ValueError):
         O.add(_rand(4), _rand(5))
+
+
+# ------------------------------------------- fused workloads
+
+@pytest.mark.parametrize("m", [1, 3, 32, 1024])
+@pytest.mark.parametrize("cls", ["U", "ONES", "RIPPLE", "RUNS", "SPARSE"])
+def test_fused_python_int(m, cls):
+    """6-Add = 4A + 3B and Poly = (A A + B)(B B + B) + A B, both mod 2^(32m),
+    against Python's arbitrary-precision ints (R17/R18)."""
+    n = 5 if m <= 32 else 2
+    a, b = inputs.make_operands(n, m, seed=m + len(cls), cls=cls)
+    a, b = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    mod = 1 << (32 * m)
+    ai, bi = rows_to_ints(a), rows_to_ints(b)
+    assert rows_to_ints(O.add6(a, b)) == [(4 * x + 3 * y) % mod for x, y in zip(ai, bi)]
+    assert rows_to_ints(O.poly(a, b, nthreads=2)) == \
+        [((x * x + y) * (y * y + y) + x * y) % mod for x, y in zip(ai, bi)]
+
+
+def test_fused_exhaustive_alphabet_one_limb():
+    """m = 1: all 256 alphabet pairs against u64 arithmetic mod 2^32."""
+    pairs = [(x, y) for x in ALPHABET for y in ALPHABET]
+    a = np.array([[x] for x, _ in pairs], dtype=np.uint32)
+    b = np.array([[y] for _, y in pairs], dtype=np.uint32)
+    M = 1 << 32
+    want6 = [(4 * x + 3 * y) % M for x, y in pairs]
+    wantp = [((x * x + y) % M * ((y * y + y) % M) + x * y) % M for x, y in pairs]
+    assert O.add6(a, b)[:, 0].tolist() == want6
+    assert O.poly(a, b)[:, 0].tolist() == wantp
+
+
+@pytest.mark.parametrize("m", [4, 128])
+def test_fused_closed_forms(m):
+    """Special cases with closed forms: a = b = 2^B - 1 = -1 (mod 2^B):
+    6-Add = -7, Poly = (1 - 1)(1 - 1) + 1 = 1; b = 0: 6-Add = 4a, Poly = 0;
+    a = 0: Poly = b^3 + b^2; b = 1: Poly = 2a^2 + a + 2."""
+    rng = np.random.default_rng(m)
+    a = rng.integers(0, 2**32, size=(3, m), dtype=np.uint64).astype(np.uint32)
+    ones = np.full_like(a, 0xFFFFFFFF)
+    zero = np.zeros_like(a)
+    one = zero.copy()
+    one[:, 0] = 1
+    mod = 1 << (32 * m)
+    assert rows_to_ints(O.add6(ones, ones)) == [mod - 7] * 3
+    assert np.array_equal(O.poly(ones, ones), one)
+    assert rows_to_ints(O.add6(a, zero)) == [4 * x % mod for x in rows_to_ints(a)]
+    assert not O.poly(a, zero).any()
+    assert rows_to_ints(O.poly(zero, a)) == [(y ** 3 + y ** 2) % mod for y in rows_to_ints(a)]
+    assert rows_to_ints(O.poly(a, one)) == [(2 * x * x + x + 2) % mod for x in rows_to_ints(a)]
