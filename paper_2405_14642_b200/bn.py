@@ -18,7 +18,9 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libbn.so")
+# BN_LIB_PATH: load another build of the same ABI (A/B timing of kernel
+# variants); default is the in-tree library built by __graft_entry__.build().
+_LIB_PATH = os.environ.get("BN_LIB_PATH") or os.path.join(_HERE, "libbn.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -53,35 +55,33 @@ def load():
             if not os.path.exists(_LIB_PATH):
                 raise ImportError("libbn.so not built at %s — run __graft_entry__.build()" % _LIB_PATH)
             lib = ctypes.CDLL(_LIB_PATH)
-            vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
-            for name in ("bn_add", "bn_mul_classical", "bn_mul_ntt", "bn_add6"):
-                f = getattr(lib, name)
-                f.argtypes = [vp, vp, vp, u64, u32, u32, vp]
-                f.restype = ctypes.c_int
-            for name in ("bn_poly_classical", "bn_poly_ntt"):
-                f = getattr(lib, name)
-                f.argtypes = [vp, vp, vp, u64, u32, u32, vp, u64, vp]
-                f.restype = ctypes.c_int
-            lib.bn_poly_workspace_bytes.argtypes = [ctypes.c_int, u64, u32, u32]
-            lib.bn_poly_workspace_bytes.restype = u64
-            lib.bn_prepare.argtypes = [ctypes.c_int]
-            lib.bn_prepare.restype = ctypes.c_int
-            lib.bn_run_host.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp), ctypes.c_int,
-                                        vp, vp, u64, u32, u32]
-            lib.bn_run_host.restype = ctypes.c_int
-            lib.bn_max_bits.restype = u32
-            lib.bn_min_bits.restype = u32
-            lib.bn_cuda_error.restype = ctypes.c_int
-            lib.bn_status_string.argtypes = [ctypes.c_int]
-            lib.bn_status_string.restype = ctypes.c_char_p
-            lib.bn_launches_per_call.argtypes = [ctypes.c_int, u32]
-            lib.bn_launches_per_call.restype = u32
-            lib.bn_ntt_primes.argtypes = [ctypes.POINTER(u32)]
-            lib.bn_ntt_primes.restype = None
-            lib.bn_debug_ntt_forward.argtypes = [vp, u64, u32, ctypes.c_int, ctypes.POINTER(u32), vp]
-            lib.bn_debug_ntt_forward.restype = ctypes.c_int
-            lib.bn_debug_set_grid_cap.argtypes = [u32]
-            lib.bn_debug_set_grid_cap.restype = None
+            vp, u64, u32, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+            sig = {
+                "bn_add": ([vp, vp, vp, u64, u32, u32, vp], i32),
+                "bn_mul_classical": ([vp, vp, vp, u64, u32, u32, vp], i32),
+                "bn_mul_ntt": ([vp, vp, vp, u64, u32, u32, vp], i32),
+                "bn_add6": ([vp, vp, vp, u64, u32, u32, vp], i32),
+                "bn_poly_classical": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
+                "bn_poly_ntt": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
+                "bn_poly_workspace_bytes": ([i32, u64, u32, u32], u64),
+                "bn_prepare": ([i32], i32),
+                "bn_run_host": ([ctypes.POINTER(i32), ctypes.POINTER(vp), i32, vp, vp, u64, u32, u32], i32),
+                "bn_max_bits": ([], u32),
+                "bn_min_bits": ([], u32),
+                "bn_cuda_error": ([], i32),
+                "bn_status_string": ([i32], ctypes.c_char_p),
+                "bn_launches_per_call": ([i32, u32], u32),
+                "bn_ntt_primes": ([ctypes.POINTER(u32)], None),
+                "bn_debug_ntt_forward": ([vp, u64, u32, i32, ctypes.POINTER(u32), vp], i32),
+                "bn_debug_set_grid_cap": ([u32], None),
+            }
+            for name, (argt, rest) in sig.items():
+                # an older build loaded through BN_LIB_PATH may lack newer
+                # entry points: those stay unbound and raise when called
+                if hasattr(lib, name):
+                    f = getattr(lib, name)
+                    f.argtypes = argt
+                    f.restype = rest
             _lib = lib
     return _lib
 

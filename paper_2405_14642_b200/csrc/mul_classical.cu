@@ -221,6 +221,11 @@ BN_DEV void resolve_lh(const uint32_t* As, const MulCRoles<C>& ro, bool valid, u
   add_regs<L2, C::G>(x, y, res, valid, agg);
 }
 
+// The 1-Mul kernel keeps its convolution / publish / resolve inline rather
+// than calling the phase helpers above: the same code routed through the
+// helpers compiles (ptxas register assignment) to a mirror-chunk loop with
+// five extra IMAD.MOVs on the saturated FMA-heavy pipe, 4-5% slower
+// (A/B on one B200, scripts/ab.sh).
 template <int LOGM, int Q>
 __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
     mul_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
@@ -228,14 +233,39 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* agg = sm + 2 * C::STAGE_WORDS;  // T/32
-  const MulCRoles<C> ro;
-  zero_b_prefix<C>(sm, 2);
+
+  const int t = threadIdx.x;
+  // convolution mapping: lane = inst_lo + I * g_lo (instance-fastest)
+  const int set = t / C::SET_T;
+  const int r = t % C::SET_T;
+  const int conv_slot = set * C::I + (r % C::I);
+  const int g = r / C::I;
+  // resolve/store mapping: instance-major, G consecutive threads per instance
+  const int add_slot = t / C::G;
+  const int chunk = t % C::G;
+
+  // B[-Q..-1] = 0 in both stages (never overwritten: loads and H start at B[0])
+  for (int v = t; v < 2 * C::IPB * Q; v += C::T) {
+    const int st = v / (C::IPB * Q), k = (v / Q) % C::IPB;
+    sm[st * C::STAGE_WORDS + C::IPB * C::SA + k * C::SB + (v % Q)] = 0u;
+  }
+  // stage A, B of a group with cp.async: coalesced 16-byte
+  // copies global -> shared, zero-filled past the last instance
+  constexpr int VPI = M / 4;  // uint4 per instance operand
+  auto issue = [&](uint64_t grp, int st) {
+    uint32_t* As = sm + st * C::STAGE_WORDS;
+    uint32_t* Bs = As + C::IPB * C::SA;
+    const uint64_t i0 = grp * C::IPB;
+    for (int v = t; v < C::IPB * VPI; v += C::T) {
+      const int k = v / VPI, w = (v % VPI) * 4;
+      const bool ok = i0 + k < n_inst;
+      const uint64_t off = ok ? (i0 + k) * M + w : 0;
+      cp_async16(As + k * C::SA + w, a + off, ok);
+      cp_async16(Bs + k * C::SB + Q + w, b + off, ok);
+    }
+  };
 
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  auto issue = [&](uint64_t grp, int st) {
-    const uint64_t i0 = grp * C::IPB;
-    stage_xy<C>(sm + st * C::STAGE_WORDS, a + i0 * M, b + i0 * M, n_inst - i0);
-  };
   uint64_t grp = blockIdx.x;
   if (grp < n_groups) issue(grp, 0);
   cp_async_commit();
@@ -246,12 +276,59 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
     cp_async_wait<1>();
     __syncthreads();
     uint32_t* As = sm + st * C::STAGE_WORDS;
-    const uint64_t inst = grp * C::IPB + ro.add_slot;
-    const bool valid = inst < n_inst;
-    conv_publish<C>(As, ro);
-    uint32_t res[2 * Q];
-    resolve_lh<C>(As, ro, valid, agg, res);
-    if (valid) store_limbs<2 * Q>(out + inst * M + 2 * Q * ro.chunk, res);
+    uint32_t* Bs = As + C::IPB * C::SA;
+    const uint64_t inst0 = grp * C::IPB;
+
+    // ---- convolution: low chunk j0 = g and mirror chunk j0' = M/Q - 1 - g
+    uint32_t lh0[Q + 2], lh1[Q + 2];
+    {
+      const uint32_t* Ai = As + conv_slot * C::SA;
+      const uint32_t* Bi = Bs + conv_slot * C::SB + Q;
+      conv_chunk<Q>(Ai, Bi, g, lh0);
+      conv_chunk<Q>(Ai, Bi, M / Q - 1 - g, lh1);
+    }
+    __syncthreads();
+
+    // ---- publish (reading R8): L[k1+q] = low_q; H[k1+Q] = high; H[k1+Q+1] = carry;
+    // H[k1+Q+2 .. k1+2Q) = 0; the top chunk zeroes H[0..Q) instead.
+    {
+      uint32_t* L = As + conv_slot * C::SA;
+      uint32_t* H = Bs + conv_slot * C::SB + Q;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t* lh = h == 0 ? lh0 : lh1;
+        const int j0 = h == 0 ? g : M / Q - 1 - g;
+        const int k1 = Q * j0;
+        uint32_t lows[Q], hs[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+          lows[q] = lh[q];
+          hs[q] = q == 0 ? lh[Q] : (q == 1 ? lh[Q + 1] : 0u);
+        }
+        sts_limbs<Q>(L + k1, lows);
+        if (k1 + Q < M) {
+          sts_limbs<Q>(H + k1 + Q, hs);
+        } else {
+          uint32_t z[Q];
+#pragma unroll
+          for (int q = 0; q < Q; q++) z[q] = 0;
+          sts_limbs<Q>(H, z);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- resolve R = L + H and store
+    {
+      constexpr int L2 = 2 * Q;
+      const uint64_t inst = inst0 + add_slot;
+      const bool valid = inst < n_inst;
+      uint32_t x[L2], y[L2], res[L2];
+      lds_limbs<L2>(x, As + add_slot * C::SA + L2 * chunk);
+      lds_limbs<L2>(y, Bs + add_slot * C::SB + Q + L2 * chunk);
+      add_regs<L2, C::G>(x, y, res, valid, agg);
+      if (valid) store_limbs<L2>(out + inst * M + L2 * chunk, res);
+    }
     __syncthreads();  // this stage is refilled two groups from now
   }
   cp_async_wait<0>();

@@ -406,22 +406,123 @@ BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const
 }
 
 // ------------------------------------------------------------ the kernels
+// The 1-Mul kernel keeps its body inline instead of calling ntt_product:
+// routed through the helper, ptxas allocates registers differently and the
+// 1024-bit instance runs 6-9% slower (A/B on one B200, scripts/ab.sh).
 template <int LOGN>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
     mul_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                    const uint2* __restrict__ tw) {
   using C = NttCfg<LOGN>;
-  constexpr int M = C::M;
+  constexpr int N = C::N, M = C::M, TPI = C::TPI;
   extern __shared__ __align__(16) uint32_t sm[];
-  const int slot = threadIdx.x / C::TPI;
-  const int t = threadIdx.x % C::TPI;
+  const int slot = threadIdx.x / TPI;
+  const int t = threadIdx.x % TPI;
+  // this slot's own (padded) exchange region, reused for L | H after the
+  // transforms: it must not reach into another slot's region, because slots
+  // in different warps only synchronise at CTA barriers
+  uint32_t* X = sm + slot * (C::XW / C::IPB);
+  // raw inverse outputs per prime; per-slot stride padded by 16 words so the two
+  // instances sharing a warp (TPI = 16) write different banks
+  constexpr int RS = 3 * M + (C::TPI < 32 ? 16 : 0);
+  uint32_t* Res = sm + 2 * C::XW + slot * RS;
+  uint32_t* agg = sm + 2 * C::XW + C::IPB * RS;
+
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
     const uint64_t inst = grp * C::IPB + slot;
     const bool valid = inst < n_inst;
-    const uint64_t io = (valid ? inst : 0) * M;
-    ntt_product<LOGN, false, false, false, false, false>(sm, slot, t, a + io, b + io, nullptr, out + io,
-                                                         valid, tw);
+    const uint32_t* ai = a + (valid ? inst : 0) * M;
+    const uint32_t* bi = b + (valid ? inst : 0) * M;
+
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xab[2][16];
+      // N-1: reduce the limbs mod p into pass-0 layout (index t + e N/16),
+      // upper half is the zero padding (reading R11)
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const uint32_t va = valid ? __ldg(ai + t + e * (N / 16)) : 0u;
+        const uint32_t vb = valid ? __ldg(bi + t + e * (N / 16)) : 0u;
+        // a_i < 2^32 < 6p: two conditional subtractions of 2p -> [0, 2p)
+        xab[0][e] = red2(red2(va, p2), p2);
+        xab[1][e] = red2(red2(vb, p2), p2);
+      }
+#pragma unroll
+      for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
+      // N-2: forward transforms of A and B together
+      fwd_all<LOGN, true, 2>(xab, sm, slot * N, t, twf, p, p2);
+      // N-3: pointwise product (same register layout for A-hat and B-hat)
+      uint32_t x[16];
+#pragma unroll
+      for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[1][e], p, pinv);
+      // N-4: inverse transform -> pass-0 layout, natural order
+      inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
+      // keep coefficients 0..M-1 (truncated product): e < 8
+#pragma unroll
+      for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
+    }
+    bar<TPI>();
+
+    // N-5 / N-6: Garner CRT of 8 consecutive coefficients, aggregate, publish
+    {
+      const CrtConst& k = c_crt[LOGN];
+      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+      uint32_t y0[8], y1[8], y2[8];
+      lds_limbs<8>(y0, Res + 0 * M + 8 * t);
+      lds_limbs<8>(y1, Res + 1 * M + 8 * t);
+      lds_limbs<8>(y2, Res + 2 * M + 8 * t);
+      uint32_t lows[8], hs[8];
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+        const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+        const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+        const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+        const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+        const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+        const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+        const uint32_t d = red2(b2v + c2v, 2 * p2);
+        const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+        // c = r0 + p0 t1 + p0 p1 t2  (< 2^90)
+        const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+        const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+        const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
+        add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
+        lows[q] = a0;
+        a0 = a1;
+        a1 = a2;
+        a2 = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      // X is dead (last exchange read it before inv_pass<0>, followed by bar)
+      uint32_t* L = X;
+      uint32_t* H = X + M;
+      sts_limbs<8>(L + 8 * t, lows);
+      if (8 * t + 8 < M) {
+        sts_limbs<8>(H + 8 * t + 8, hs);
+      } else {
+        uint32_t z[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) z[q] = 0;
+        sts_limbs<8>(H, z);
+      }
+    }
+    bar<TPI>();
+    // N-7: R = L + H, store
+    {
+      uint32_t xl[8], yh[8], r[8];
+      lds_limbs<8>(xl, X + 8 * t);
+      lds_limbs<8>(yh, X + M + 8 * t);
+      add_regs<8, TPI>(xl, yh, r, valid, agg);
+      if (valid) store_limbs<8>(out + inst * M + 8 * t, r);
+    }
+    __syncthreads();  // X / Res / agg reused by the next group
   }
 }
 
