@@ -370,7 +370,9 @@ def fused_rates(name: str, ms: float, total_inst: int, w):
     over 3*bits/8 bytes (the footnote's ideal: read a, b, write one result);
     Poly as 4 multiplications (mults/s) and 4x the 1-Mul Gu32ops count."""
     r = {"ms": ms}
-    if name == "add6":
+    if name.startswith("mul_wide"):
+        r["mults/s"] = total_inst / (ms * 1e-3)
+    elif name == "add6":
         r["GB/s"] = total_inst * w["add_bytes"] / (ms * 1e-3) / 1e9
         r["add6/s"] = total_inst / (ms * 1e-3)
     else:
@@ -381,9 +383,14 @@ def fused_rates(name: str, ms: float, total_inst: int, w):
 
 
 def time_fused(bn, torch, a, b, out, stream, steps, n, world, w, max_over_ranks, barrier):
-    """NEXT rows, timed after the step on the same inputs:
+    """NEXT rows (SURVEY §8(f) #1 fused 6-Add / Poly, #2 full products),
+    timed after the step on the same inputs:
     each op `steps` times back to back, CUDA events on the launch stream."""
-    fns = {"add6": lambda: bn.add6(a, b, out=out)}
+    wide_out = torch.empty((a.shape[0], 2 * a.shape[1]), dtype=a.dtype, device=a.device)
+    fns = {"add6": lambda: bn.add6(a, b, out=out),
+           "mul_wide_classical": lambda: bn.mul_wide_classical(a, b, out=wide_out)}
+    if a.shape[1] * 32 <= 131072:
+        fns["mul_wide_ntt"] = lambda: bn.mul_wide_ntt(a, b, out=wide_out)
     for name, f in (("poly_classical", bn.poly_classical), ("poly_ntt", bn.poly_ntt)):
         ws = bn.poly_workspace(name, a)
         fns[name] = (lambda f=f, ws=ws: f(a, b, out=out, workspace=ws))
@@ -429,11 +436,15 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
         fns = [("add", bn.add), ("mul_classical", bn.mul_classical), ("mul_ntt", bn.mul_ntt)]
         if not args.no_fused:
             wsc, wsn = bn.poly_workspace("poly_classical", a), bn.poly_workspace("poly_ntt", a)
+            wo = torch.empty((n, 2 * m), dtype=a.dtype, device=dev)
+            fns += [("mul_wide_classical", lambda x, y, out: bn.mul_wide_classical(x, y, out=wo))]
+            if bits <= 131072:
+                fns += [("mul_wide_ntt", lambda x, y, out: bn.mul_wide_ntt(x, y, out=wo))]
             fns += [("add6", bn.add6),
                     ("poly_classical", lambda x, y, out: bn.poly_classical(x, y, out=out, workspace=wsc)),
                     ("poly_ntt", lambda x, y, out: bn.poly_ntt(x, y, out=out, workspace=wsn))]
         for name, f in fns:
-            slow = name in ("mul_classical", "poly_classical") and bits > 32768
+            slow = name in ("mul_classical", "poly_classical", "mul_wide_classical") and bits > 32768
             reps = 3 if slow else 20
             for _ in range(2):
                 f(a, b, out=o)
@@ -448,7 +459,7 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
             ms = max_over_ranks(e0.elapsed_time(e1) / reps)
             tot = n * world
             row = {"sweep": True, "op": name, "bits": bits, "instances": tot, "ms": ms, "n_gpus": world}
-            if name in ("add6", "poly_classical", "poly_ntt"):
+            if name in ("add6", "poly_classical", "poly_ntt", "mul_wide_classical", "mul_wide_ntt"):
                 row.update(fused_rates(name, ms, tot, w))
                 if name == "add6":
                     row["frac_hbm"] = row["GB/s"] / world / peaks["hbm_gbs"]
@@ -466,6 +477,8 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
             if rank == 0:
                 print(json.dumps(row), flush=True)
         del a, b, o
+        if not args.no_fused:
+            del wo
         torch.cuda.empty_cache()
 
 

@@ -130,6 +130,22 @@ bn_status bn_poly_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
  * n_inst == 0 or invalid arguments.  May initialise the device (bn_prepare). */
 uint64_t bn_poly_workspace_bytes(int op, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
 
+/* ---- full (untruncated) products -------------------------
+ * bn_mul_wide_classical / bn_mul_wide_ntt — out[k] = a[k] * b[k] exactly, as
+ * 2*n_limbs limbs of limb_bits (Eq. 1, without the k < M
+ * truncation: all columns 0 <= k < 2M).  out holds n_inst * 2 * n_limbs
+ * limbs and may not overlap a or b at all (it is twice their size); a and b
+ * follow bn_add's rules.  Classical: the truncated kernel's partition for
+ * the low half and the same convolution on mirrored operands for the high
+ * half; bits in [1024, 262144].  NTT: the N = 2m point
+ * transforms already produce every coefficient; bits in [1024, 131072]
+ * (a 262144-bit input returns BN_ESIZE: its 3N residues do not fit one
+ * CTA's shared memory next to the exchange planes). */
+bn_status bn_mul_wide_classical(void *out, const void *a, const void *b, uint64_t n_inst,
+                                uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
+bn_status bn_mul_wide_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
+                          uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
+
 /* Build the NTT twiddle/CRT tables for `device` (all sizes), synchronously.
  * Idempotent and thread-safe; bn_mul_ntt calls it lazily. */
 bn_status bn_prepare(int device);
@@ -146,7 +162,10 @@ bn_status bn_prepare(int device);
  * Device scratch is allocated on first use and cached per device (grown on
  * demand).  Synchronous: returns when every output is in host memory. */
 enum { BN_OP_ADD = 0, BN_OP_MUL_CLASSICAL = 1, BN_OP_MUL_NTT = 2, BN_OP_ADD6 = 3,
-       BN_OP_POLY_CLASSICAL = 4, BN_OP_POLY_NTT = 5 };
+       BN_OP_POLY_CLASSICAL = 4, BN_OP_POLY_NTT = 5,
+       /* not accepted by bn_run_host (output is twice the size); used by
+        * bn_launches_per_call */
+       BN_OP_MUL_WIDE_CLASSICAL = 6, BN_OP_MUL_WIDE_NTT = 7 };
 bn_status bn_run_host(const int *ops, void *const *outs, int n_ops, const void *a,
                       const void *b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
 

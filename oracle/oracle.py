@@ -117,6 +117,15 @@ def add_carry(a, b):
     return out, int(c)
 
 
+def mul_full_rows(a, b) -> np.ndarray:
+    """Per instance (rows) the full 2m-limb product (oracle_mul_full)."""
+    a, b = _as2d(a), _as2d(b)
+    out = np.empty((a.shape[0], 2 * a.shape[1]), dtype=np.uint32)
+    for i in range(a.shape[0]):
+        out[i] = mul_full(a[i], b[i])
+    return out
+
+
 def mul_full(a, b) -> np.ndarray:
     """One instance: the full 2m-limb product."""
     a = np.ascontiguousarray(a, dtype=np.uint32).ravel()

@@ -31,7 +31,8 @@ _STATUS = {0: "BN_OK", 1: "BN_EINVAL", 2: "BN_ESIZE", 3: "BN_EALIGN", 4: "BN_EAL
 
 OP_ADD, OP_MUL_CLASSICAL, OP_MUL_NTT, OP_ADD6, OP_POLY_CLASSICAL, OP_POLY_NTT = 0, 1, 2, 3, 4, 5
 OPS = {"add": OP_ADD, "mul_classical": OP_MUL_CLASSICAL, "mul_ntt": OP_MUL_NTT, "add6": OP_ADD6,
-       "poly_classical": OP_POLY_CLASSICAL, "poly_ntt": OP_POLY_NTT}
+       "poly_classical": OP_POLY_CLASSICAL, "poly_ntt": OP_POLY_NTT, "mul_wide_classical": 6,
+       "mul_wide_ntt": 7}
 
 
 class BnError(RuntimeError):
@@ -61,6 +62,8 @@ def load():
                 "bn_mul_classical": ([vp, vp, vp, u64, u32, u32, vp], i32),
                 "bn_mul_ntt": ([vp, vp, vp, u64, u32, u32, vp], i32),
                 "bn_add6": ([vp, vp, vp, u64, u32, u32, vp], i32),
+                "bn_mul_wide_classical": ([vp, vp, vp, u64, u32, u32, vp], i32),
+                "bn_mul_wide_ntt": ([vp, vp, vp, u64, u32, u32, vp], i32),
                 "bn_poly_classical": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
                 "bn_poly_ntt": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
                 "bn_poly_workspace_bytes": ([i32, u64, u32, u32], u64),
@@ -142,6 +145,34 @@ def mul_classical(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
 def mul_ntt(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
     """(a * b) mod 2^bits per instance, exact 3-prime NTT (bn_mul_ntt)."""
     return _call("bn_mul_ntt", a, b, out)
+
+
+def _wide(name: str, a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    _check(a, b, a)  # operand checks only
+    n_inst, n_limbs = a.shape
+    if out is None:
+        out = torch.empty((n_inst, 2 * n_limbs), dtype=a.dtype, device=a.device)
+    elif out.shape != (n_inst, 2 * n_limbs) or out.dtype != a.dtype or out.device != a.device \
+            or not out.is_contiguous():
+        raise ValueError("out must be [n_inst, 2*n_limbs], a's dtype and device, contiguous")
+    lib = load()
+    with torch.cuda.device(a.device):
+        stream = torch.cuda.current_stream(a.device).cuda_stream
+        st = getattr(lib, name)(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs,
+                                _limb_bits(a), stream)
+    if st != 0:
+        raise BnError(st, name)
+    return out
+
+
+def mul_wide_classical(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    """Full product a * b (2 n_limbs limbs per instance), quadratic algorithm."""
+    return _wide("bn_mul_wide_classical", a, b, out)
+
+
+def mul_wide_ntt(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+    """Full product a * b (2 n_limbs limbs per instance), exact NTT; bits <= 131072."""
+    return _wide("bn_mul_wide_ntt", a, b, out)
 
 
 def add6(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:

@@ -269,6 +269,37 @@ bn_status run_op(int op, void* out, const void* a, const void* b, uint64_t n_ins
   return e == cudaSuccess ? BN_OK : cuda_fail(e);
 }
 
+// Full products: out holds 2 n_limbs limbs per instance (partial overlap with
+// an input is rejected; out may not equal an input either, it is twice as large)
+bn_status run_wide(int op, void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+                   uint32_t limb_bits, cudaStream_t st) {
+  int logm = 0;
+  // operand checks (out is checked below against its doubled size)
+  bn_status s = validate(a, a, a, n_inst, n_limbs, limb_bits, &logm);
+  if (s != BN_OK) return s;
+  if (n_inst && !b) return BN_EINVAL;
+  if (n_inst && ((uintptr_t)b & 15)) return BN_EALIGN;
+  if (op == BN_OP_MUL_WIDE_NTT && logm > 12) return BN_ESIZE;
+  if (n_inst == 0) return BN_OK;
+  if (!out) return BN_EINVAL;
+  if ((uintptr_t)out & 15) return BN_EALIGN;
+  const uint64_t bytes = n_inst * ((uint64_t)n_limbs * limb_bits / 8);
+  auto overl = [](const void* x, uint64_t xn, const void* y, uint64_t yn) {
+    const uintptr_t x0 = (uintptr_t)x, y0 = (uintptr_t)y;
+    return x0 < y0 + yn && y0 < x0 + xn;
+  };
+  if (overl(out, 2 * bytes, a, bytes) || overl(out, 2 * bytes, b, bytes)) return BN_EALIAS;
+  DevState* d = nullptr;
+  s = current_device(&d);
+  if (s != BN_OK) return s;
+  cudaError_t e = op == BN_OP_MUL_WIDE_CLASSICAL
+                      ? bn::launch_mul_wide_classical(logm, (uint32_t*)out, (const uint32_t*)a,
+                                                      (const uint32_t*)b, n_inst, st, d->n_sm)
+                      : bn::launch_mul_wide_ntt(logm, (uint32_t*)out, (const uint32_t*)a, (const uint32_t*)b,
+                                                n_inst, d->tables[logm + 1], st, d->n_sm);
+  return e == cudaSuccess ? BN_OK : cuda_fail(e);
+}
+
 bool is_poly(int op) { return op == BN_OP_POLY_CLASSICAL || op == BN_OP_POLY_NTT; }
 
 // workspace words of a Poly call (one slice per resident CTA of its grid)
@@ -332,6 +363,16 @@ bn_status bn_mul_ntt(void* out, const void* a, const void* b, uint64_t n_inst, u
 bn_status bn_add6(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits,
                   bn_stream_t stream) {
   return run_op(BN_OP_ADD6, out, a, b, n_inst, n_limbs, limb_bits, (cudaStream_t)stream);
+}
+
+bn_status bn_mul_wide_classical(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+                                 uint32_t limb_bits, bn_stream_t stream) {
+  return run_wide(BN_OP_MUL_WIDE_CLASSICAL, out, a, b, n_inst, n_limbs, limb_bits, (cudaStream_t)stream);
+}
+
+bn_status bn_mul_wide_ntt(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+                          uint32_t limb_bits, bn_stream_t stream) {
+  return run_wide(BN_OP_MUL_WIDE_NTT, out, a, b, n_inst, n_limbs, limb_bits, (cudaStream_t)stream);
 }
 
 uint64_t bn_poly_workspace_bytes(int op, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits) {
@@ -470,9 +511,10 @@ const char* bn_status_string(bn_status s) {
 }
 
 uint32_t bn_launches_per_call(int op, uint32_t bits) {
-  if (op < BN_OP_ADD || op > BN_OP_POLY_NTT) return 0;
+  if (op < BN_OP_ADD || op > BN_OP_MUL_WIDE_NTT) return 0;
   const int lb = ilog2_exact(bits);
   if (lb < 10 || lb > 18) return 0;
+  if (op == BN_OP_MUL_WIDE_NTT && lb > 17) return 0;
   return 1;
 }
 

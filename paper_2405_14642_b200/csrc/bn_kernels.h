@@ -67,6 +67,12 @@ cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, co
 cudaError_t poly_ntt_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words);
 cudaError_t launch_poly_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                             const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st, int n_sm);
+// Full (untruncated) products: out has 2^(logm+1) u32 limbs per instance.
+// The NTT version supports logm <= 12 (inputs up to 128K bits).
+cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                      uint64_t n_inst, cudaStream_t st, int n_sm);
+cudaError_t launch_mul_wide_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm);
 cudaError_t launch_ntt_forward_debug(int lgn, uint32_t* x, uint64_t n_inst, int prime,
                                      const NttTables& tb, cudaStream_t st);
 

@@ -80,7 +80,11 @@ BN_DEV void mac_block(uint32_t (&lo)[Q], uint32_t (&hi)[Q], uint32_t (&top)[Q], 
 // B[-Q..-1] == 0.  Block c covers i in [Q c, Q c + Q) against B chunks
 // j0 - c (cur) and j0 - c - 1 (prev); two blocks per trip so the window
 // registers swap roles instead of being copied.
-template <int Q>
+// REV: the staged operands are the reversed ones of the wide product's high
+// half (mul_wide_classical_kernel), whose column Q j0 + q is the original
+// column 2M - 1 - Q j0 - q: combine then runs over q descending so lhcs is
+// in ascending original order.
+template <int Q, bool REV = false>
 BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_t (&lhcs)[Q + 2]) {
   uint32_t lo[Q], hi[Q], top[Q];
 #pragma unroll
@@ -107,14 +111,16 @@ BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_
     mac_block<Q>(lo, hi, top, av, b0, b1);
   }
   // combine: accum = (lo, hi), carry = top
-  lhcs[0] = lo[0];
-  uint32_t h_res = hi[0], c_res = top[0];
+  constexpr int F = REV ? Q - 1 : 0;
+  lhcs[0] = lo[F];
+  uint32_t h_res = hi[F], c_res = top[F];
 #pragma unroll
   for (int q = 1; q < Q; q++) {
-    const uint32_t l = lo[q], h = hi[q];
+    const int x = REV ? Q - 1 - q : q;
+    const uint32_t l = lo[x], h = hi[x];
     lhcs[q] = l + h_res;
     h_res = h + (c_res + (lhcs[q] < l));
-    c_res = top[q] + (h_res < h);
+    c_res = top[x] + (h_res < h);
   }
   lhcs[Q] = h_res;
   lhcs[Q + 1] = c_res;
@@ -400,6 +406,149 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
   }
 }
 
+// ------------------------------------------------------------ full product
+// Wide (untruncated) product: out[k] = a[k] * b[k] as 2M
+// limbs, C_k = sum_{i+j=k} A_i B_j for 0 <= k < 2M (Eq. 1 without the
+// k < M truncation).  The low half is exactly the truncated kernel's work.
+// The high half uses the mirror identity: with A''_i = A_{M-i} (A''_0 = 0)
+// and B'_j = B_{M-1-j}, column K < M of the truncated A'' B' equals the
+// original column 2M-1-K, so the same conv_chunk (with a reversed combine)
+// computes it; Fig. 5's load balance carries over, each thread owning the
+// chunk pairs (g, M/Q-1-g) of both halves.  L / H span 2M words (reading R8
+// with M -> 2M) and one scan-add resolves 2M limbs.
+template <int LOGM, int Q_>
+struct MulWCfg {
+  using B = MulCCfg<LOGM, Q_>;
+  static constexpr int M = B::M, Q = Q_, G = B::G, I = B::I, SET_T = B::SET_T, T = B::T, IPB = B::IPB;
+  static constexpr int SA = 2 * M + 4;  // A | A''   (L afterwards)
+  // B region: Q zeros | B | Q zeros | B' ; H = [Q, Q + 2M) afterwards
+  static constexpr int SB = 2 * M + 2 * Q + (((4 * B::BS - 2 * Q) % 32) + 32) % 32;
+  static constexpr int STAGE_WORDS = IPB * (SA + SB);
+  static constexpr int SMEM_WORDS = STAGE_WORDS + T / 32;
+  static constexpr int MINB = B::MINB;
+};
+
+template <int LOGM, int Q>
+__global__ void __launch_bounds__(MulWCfg<LOGM, Q>::T, MulWCfg<LOGM, Q>::MINB)
+    mul_wide_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
+  using C = MulWCfg<LOGM, Q>;
+  constexpr int M = C::M;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* As = sm;
+  uint32_t* Bs = sm + C::IPB * C::SA;
+  uint32_t* agg = sm + C::STAGE_WORDS;
+  const int t = threadIdx.x;
+  const int set = t / C::SET_T;
+  const int r = t % C::SET_T;
+  const int conv_slot = set * C::I + (r % C::I);
+  const int g = r / C::I;
+  const int add_slot = t / C::G;
+  const int chunk = t % C::G;
+  constexpr int VPI = M / 4;
+
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t i0 = grp * C::IPB;
+    // stage A -> As[k][0, M), B -> Bs[k][Q, Q + M)
+    for (int v = t; v < C::IPB * VPI; v += C::T) {
+      const int k = v / VPI, w = (v % VPI) * 4;
+      const bool ok = i0 + k < n_inst;
+      const uint64_t off = ok ? (i0 + k) * M + w : 0;
+      cp_async16(As + k * C::SA + w, a + off, ok);
+      cp_async16(Bs + k * C::SB + Q + w, b + off, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // mirrored copies: A''_i = A_{M-i} (A''_0 = 0) at As[M + i]; B'_j =
+    // B_{M-1-j} at Bs[2Q + M + j]; zero prefixes Bs[0, Q) and Bs[Q+M, 2Q+M)
+    for (int v = t; v < C::IPB * M; v += C::T) {
+      const int k = v / M, i = v % M;
+      uint32_t* Ak = As + k * C::SA;
+      uint32_t* Bk = Bs + k * C::SB;
+      Ak[M + i] = i == 0 ? 0u : Ak[M - i];
+      Bk[2 * Q + M + i] = Bk[Q + M - 1 - i];
+      if (i < Q) {
+        Bk[i] = 0u;
+        Bk[Q + M + i] = 0u;
+      }
+    }
+    __syncthreads();
+
+    // ---- convolution: low pair (A, B) and high pair (A'', B')
+    uint32_t lh[4][Q + 2];
+    {
+      const uint32_t* Ai = As + conv_slot * C::SA;
+      const uint32_t* Bi = Bs + conv_slot * C::SB + Q;
+      conv_chunk<Q>(Ai, Bi, g, lh[0]);
+      conv_chunk<Q>(Ai, Bi, M / Q - 1 - g, lh[1]);
+      conv_chunk<Q, true>(Ai + M, Bi + M + Q, g, lh[2]);
+      conv_chunk<Q, true>(Ai + M, Bi + M + Q, M / Q - 1 - g, lh[3]);
+    }
+    __syncthreads();
+    // ---- publish over 2M columns: L = As[k][0, 2M), H = Bs[k][Q, Q + 2M)
+    {
+      uint32_t* L = As + conv_slot * C::SA;
+      uint32_t* H = Bs + conv_slot * C::SB + Q;
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        const int j0 = (h & 1) == 0 ? g : M / Q - 1 - g;
+        // low chunks start at Q j0; high K-chunk j0 covers original columns
+        // [2M - Q (j0 + 1), 2M - Q j0)
+        const int k1 = h < 2 ? Q * j0 : 2 * M - Q * (j0 + 1);
+        uint32_t lows[Q], hs[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+          lows[q] = lh[h][q];
+          hs[q] = q == 0 ? lh[h][Q] : (q == 1 ? lh[h][Q + 1] : 0u);
+        }
+        sts_limbs<Q>(L + k1, lows);
+        if (k1 + Q < 2 * M) {
+          sts_limbs<Q>(H + k1 + Q, hs);
+        } else {
+          uint32_t z[Q];
+#pragma unroll
+          for (int q = 0; q < Q; q++) z[q] = 0;
+          sts_limbs<Q>(H, z);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- resolve R = L + H over 2M limbs (4Q per thread) and store
+    {
+      constexpr int L4 = 4 * Q;
+      const uint64_t inst = i0 + add_slot;
+      const bool valid = inst < n_inst;
+      uint32_t x[L4], y[L4], res[L4];
+      lds_limbs<L4>(x, As + add_slot * C::SA + L4 * chunk);
+      lds_limbs<L4>(y, Bs + add_slot * C::SB + Q + L4 * chunk);
+      add_regs<L4, C::G>(x, y, res, valid, agg);
+      if (valid) store_limbs<L4>(out + inst * 2 * M + L4 * chunk, res);
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGM>
+static cudaError_t launch_mulw_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                 cudaStream_t st, int n_sm) {
+  constexpr int Q = 4;
+  using C = MulWCfg<LOGM, Q>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(mul_wide_classical_kernel<LOGM, Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_wide_classical_kernel<LOGM, Q>, C::T, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t cap = (uint64_t)n_sm * per_sm * 4;
+  const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
+  mul_wide_classical_kernel<LOGM, Q><<<grid, C::T, smem, st>>>(out, a, b, n_inst);
+  return cudaGetLastError();
+}
+
 template <int LOGM>
 static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                  cudaStream_t st, int n_sm) {
@@ -468,6 +617,11 @@ static cudaError_t launch_polyc_t(uint32_t* out, const uint32_t* a, const uint32
     case 13: return F<13>(__VA_ARGS__);             \
     default: return cudaErrorInvalidValue;          \
   }
+
+cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                      uint64_t n_inst, cudaStream_t st, int n_sm) {
+  BN_LOGM_SWITCH(launch_mulw_t, out, a, b, n_inst, st, n_sm)
+}
 
 cudaError_t poly_classical_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words) {
   unsigned grid = 0;

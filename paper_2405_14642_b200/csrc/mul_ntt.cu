@@ -560,6 +560,157 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
   }
 }
 
+// ------------------------------------------------------------ full product
+// Wide (untruncated) product: out[k] = a[k] * b[k] as 2m
+// limbs.  The N = 2m point transform already yields every coefficient
+// c_0..c_{2m-2} of Eq. 1 without truncation (P:338-342 with k < 2M), so the
+// wide product is the same three transforms per prime keeping all 16
+// register elements (e < 16) through the CRT; each thread then aggregates
+// 16 consecutive coefficients into 16 lows + 2 overflow words, publishes
+// them as L / H over 2m words (reading R8 with M -> 2M) and the scan-add
+// resolves 2m limbs.  Shared memory: the two exchange planes + 3N residues
+// per slot, so N <= 2^13 (inputs up to 128K bits, results up to 256K).
+template <int LOGN>
+struct NttWideCfg {
+  using B = NttCfg<LOGN>;
+  static constexpr int RS = 3 * B::N + (B::TPI < 32 ? 16 : 0);
+  static constexpr int SMEM_WORDS = 2 * B::XW + B::IPB * RS + B::T / 32;
+  static constexpr int MINB = LOGN <= 12 ? 2 : 1;  // <= 128 registers
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T, NttWideCfg<LOGN>::MINB)
+    mul_wide_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                        const uint2* __restrict__ tw) {
+  using C = NttCfg<LOGN>;
+  using W = NttWideCfg<LOGN>;
+  constexpr int N = C::N, M = C::M, TPI = C::TPI;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int slot = threadIdx.x / TPI;
+  const int t = threadIdx.x % TPI;
+  uint32_t* X = sm + slot * (C::XW / C::IPB);  // plane-0 region of the slot
+  uint32_t* X1 = X + C::XW;                      // plane-1 region of the slot
+  uint32_t* Res = sm + 2 * C::XW + slot * W::RS;
+  uint32_t* agg = sm + 2 * C::XW + C::IPB * W::RS;
+
+  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+  for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint64_t inst = grp * C::IPB + slot;
+    const bool valid = inst < n_inst;
+    const uint32_t* ai = a + (valid ? inst : 0) * M;
+    const uint32_t* bi = b + (valid ? inst : 0) * M;
+
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xab[2][16];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const uint32_t va = valid ? __ldg(ai + t + e * (N / 16)) : 0u;
+        const uint32_t vb = valid ? __ldg(bi + t + e * (N / 16)) : 0u;
+        xab[0][e] = red2(red2(va, p2), p2);
+        xab[1][e] = red2(red2(vb, p2), p2);
+      }
+#pragma unroll
+      for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
+      fwd_all<LOGN, true, 2>(xab, sm, slot * N, t, twf, p, p2);
+      uint32_t x[16];
+#pragma unroll
+      for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[1][e], p, pinv);
+      inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
+      // all N coefficients (the last, c_{N-1}, is 0)
+#pragma unroll
+      for (int e = 0; e < 16; e++) Res[j * N + t + e * (N / 16)] = x[e];
+    }
+    bar<TPI>();
+
+    // Garner CRT of 16 consecutive coefficients, aggregate, publish
+    {
+      const CrtConst& k = c_crt[LOGN];
+      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+      uint32_t lows[16];
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        uint32_t y0[8], y1[8], y2[8];
+        lds_limbs<8>(y0, Res + 0 * N + 16 * t + 8 * h);
+        lds_limbs<8>(y1, Res + 1 * N + 16 * t + 8 * h);
+        lds_limbs<8>(y2, Res + 2 * N + 16 * t + 8 * h);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+          const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+          const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+          const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+          const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+          const uint32_t d = red2(b2v + c2v, 2 * p2);
+          const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+          const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
+          add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
+          lows[8 * h + q] = a0;
+          a0 = a1;
+          a1 = a2;
+          a2 = 0;
+        }
+      }
+      uint32_t hs[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      // planes are dead (last exchange read them before the barrier above):
+      // L = plane 0 region, H = plane 1 region, N words each
+      uint32_t* L = X;
+      uint32_t* H = X1;
+      sts_limbs<16>(L + 16 * t, lows);
+      if (16 * t + 16 < N) {
+        sts_limbs<16>(H + 16 * t + 16, hs);
+      } else {
+        uint32_t z[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) z[q] = 0;
+        sts_limbs<16>(H, z);
+      }
+    }
+    bar<TPI>();
+    {
+      uint32_t xl[16], yh[16], r[16];
+      lds_limbs<16>(xl, X + 16 * t);
+      lds_limbs<16>(yh, X1 + 16 * t);
+      add_regs<16, TPI>(xl, yh, r, valid, agg);
+      if (valid) store_limbs<16>(out + inst * N + 16 * t, r);
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_wide_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                     const NttTables& tb, cudaStream_t st, int n_sm) {
+  if constexpr (LOGN > 13) {
+    return cudaErrorInvalidValue;
+  } else {
+    using C = NttCfg<LOGN>;
+    constexpr size_t smem = NttWideCfg<LOGN>::SMEM_WORDS * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(mul_wide_ntt_kernel<LOGN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_wide_ntt_kernel<LOGN>, C::T, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
+    const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
+    mul_wide_ntt_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw);
+    return cudaGetLastError();
+  }
+}
+
 // Forward transform only (tests): rows of N residues < p, in place,
 // bit-reversed output in [0, p).
 template <int LOGN>
@@ -700,6 +851,11 @@ cudaError_t launch_ntt_forward_debug(int lgn, uint32_t* x, uint64_t n_inst, int 
     case 14: return F<14>(__VA_ARGS__);   \
     default: return cudaErrorInvalidValue; \
   }
+
+cudaError_t launch_mul_wide_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm) {
+  BN_LOGN_SWITCH(launch_wide_ntt_t, out, a, b, n_inst, tb, st, n_sm)
+}
 
 cudaError_t poly_ntt_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_words) {
   unsigned grid = 0;

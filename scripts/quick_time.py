@@ -22,9 +22,11 @@ bn.prepare(0)
 for bits in [int(x) for x in args.bits.split(",")]:
     m, n = bits // 32, (1 << 32) // bits
     a, b = inputs.make_operands(n, m, seed=1, cls="U", device=dev)
-    o = torch.empty_like(a)
+    o1 = torch.empty_like(a)
+    o2 = torch.empty((n, 2 * m), dtype=a.dtype, device=dev)
     for op in args.ops.split(","):
         f = getattr(bn, op)
+        o = o2 if "wide" in op else o1
         kw = {"workspace": bn.poly_workspace(op, a)} if op.startswith("poly") else {}
         reps = args.reps if not (("classical" in op) and bits > 32768) else 3
         for _ in range(3):

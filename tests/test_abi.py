@@ -140,3 +140,17 @@ def test_poly_validation_before_launch(lib, op):
     assert lib.bn_poly_workspace_bytes(4, 10, 48, 32) == 0
     assert lib.bn_poly_workspace_bytes(0, 10, 32, 32) == 0
     assert lib.bn_poly_workspace_bytes(5, 0, 32, 32) == 0
+
+
+@pytest.mark.parametrize("op", ["bn_mul_wide_classical", "bn_mul_wide_ntt"])
+def test_wide_validation_before_launch(lib, op):
+    A, B, O = 0x10000, 0x200000, 0x4000000
+    assert _call(lib, op, O, A, B, 4, 32, 7) == 1
+    assert _call(lib, op, O, A, B, 4, 48, 32) == 2
+    assert _call(lib, op, O, A, B, 0, 32, 32) == 0
+    assert _call(lib, op, O + 4, A, B, 4, 32, 32) == 3
+    assert _call(lib, op, A, A, B, 4, 32, 32) == 4          # out == a: twice the size, overlaps
+    assert _call(lib, op, A - 16, A, B, 4, 32, 32) == 4
+    if op == "bn_mul_wide_ntt":
+        assert _call(lib, op, O, A, B, 4, 8192, 32) == 2    # 256K-bit inputs: NTT wide unsupported
+    assert lib.bn_launches_per_call(7, 262144) == 0 and lib.bn_launches_per_call(6, 262144) == 1

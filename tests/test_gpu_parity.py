@@ -366,3 +366,68 @@ def test_run_host_fused(bits):
     idx = [0, n // 2, n - 1]
     assert np.array_equal(inputs.to_numpy_u32(outs[2][idx]),
                           O.poly(inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx])))
+
+
+# ------------------------------------------- full (wide) products (§8(f) #2)
+
+@pytest.mark.parametrize("cls", ["U", "ONES", "RIPPLE", "MIX"])
+@pytest.mark.parametrize("bits", SIZES)
+def test_parity_wide(bits, cls):
+    """Full 2m-limb products vs the oracle's untruncated schoolbook product,
+    bit-exact (NTT: inputs up to 128K bits)."""
+    m = bits // 32
+    n = max(2, N_INST[bits] // 4) if bits >= 65536 else N_INST[bits]
+    a, b = inputs.make_operands(n, m, seed=7 * bits + len(cls), cls=cls)
+    want = O.mul_full_rows(inputs.to_numpy_u32(a), inputs.to_numpy_u32(b))
+    da, db = a.to(DEV), b.to(DEV)
+    got = inputs.to_numpy_u32(bn.mul_wide_classical(da, db))
+    bad = _first_bad(got, want)
+    assert bad is None, "wide classical %d bits %s: %s" % (bits, cls, bad)
+    if bits <= 131072:
+        got = inputs.to_numpy_u32(bn.mul_wide_ntt(da, db))
+        bad = _first_bad(got, want)
+        assert bad is None, "wide ntt %d bits %s: %s" % (bits, cls, bad)
+    else:
+        with pytest.raises(bn.BnError):
+            bn.mul_wide_ntt(da, db)
+
+
+@pytest.mark.parametrize("cap", [1, 4])
+@pytest.mark.parametrize("bits", [1024, 16384])
+def test_wide_grid_cap_and_u64(bits, cap):
+    m = bits // 32
+    a, b = inputs.make_operands(77, m, seed=cap, cls="MIX")
+    want = O.mul_full_rows(inputs.to_numpy_u32(a), inputs.to_numpy_u32(b))
+    da, db = a.to(DEV), b.to(DEV)
+    bn.debug_set_grid_cap(cap)
+    try:
+        for f in (bn.mul_wide_classical, bn.mul_wide_ntt):
+            assert np.array_equal(inputs.to_numpy_u32(f(da, db)), want), f.__name__
+            got = f(da.view(torch.int64), db.view(torch.int64)).view(torch.int32)
+            assert np.array_equal(inputs.to_numpy_u32(got), want), f.__name__ + " u64"
+    finally:
+        bn.debug_set_grid_cap(0)
+    with pytest.raises(bn.BnError):  # out may not overlap an input
+        big = torch.empty((77, 3 * m), dtype=torch.int32, device=DEV)
+        x = big[:, :m].contiguous()
+        bn._wide("bn_mul_wide_classical", da, db, out=None)  # fine
+        lib = bn.load()
+        st = lib.bn_mul_wide_classical(big.data_ptr(), big.data_ptr(), db.data_ptr(), 77, m, 32, None)
+        if st != 0:
+            raise bn.BnError(st, "alias")
+        del x
+
+
+def test_wide_full_size_4096():
+    """Bench-size batch: classical wide == NTT wide on all 2^20 instances, the
+    low half equals the truncated product, and sampled instances match the
+    oracle's full product."""
+    m, n = 128, 1 << 20
+    a, b = inputs.make_operands(n, m, seed=3, cls="U", device=DEV)
+    wc = bn.mul_wide_classical(a, b)
+    wn = bn.mul_wide_ntt(a, b)
+    assert torch.equal(wc, wn)
+    assert torch.equal(wc[:, :m], bn.mul_ntt(a, b))
+    idx = torch.tensor([0, 12345, n - 1], device=DEV)
+    want = O.mul_full_rows(inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx]))
+    assert np.array_equal(inputs.to_numpy_u32(wc[idx]), want)

@@ -227,3 +227,16 @@ def test_fused_closed_forms(m):
     assert not O.poly(a, zero).any()
     assert rows_to_ints(O.poly(zero, a)) == [(y ** 3 + y ** 2) % mod for y in rows_to_ints(a)]
     assert rows_to_ints(O.poly(a, one)) == [(2 * x * x + x + 2) % mod for x in rows_to_ints(a)]
+
+
+@pytest.mark.parametrize("m", [1, 2, 32, 1024])
+@pytest.mark.parametrize("cls", ["U", "ONES", "RUNS", "SPARSE"])
+def test_mul_full_python_int(m, cls):
+    """Full 2m-limb product (the wide entry points' definition) against
+    Python ints: A * B exactly, no truncation (Eq. 1 with k < 2M)."""
+    n = 3 if m <= 32 else 1
+    a, b = inputs.make_operands(n, m, seed=m + 5, cls=cls)
+    a, b = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    got = O.mul_full_rows(a, b)
+    assert got.shape == (n, 2 * m)
+    assert rows_to_ints(got) == [x * y for x, y in zip(rows_to_ints(a), rows_to_ints(b))]
