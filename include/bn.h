@@ -15,9 +15,13 @@
  * (little-endian device), so every kernel works on u32 limbs internally.
  *
  * SIZES: bits = n_limbs * limb_bits must be a power of two in
- * [1024, 262144] (the paper's 2^11..2^18 sweep, PAPER.md:919 and Tables 1-2,
- * plus 2^10).  262144 bits is the largest size whose exact NTT product fits
- * one CTA's shared memory (DESIGN.md §Data layout).
+ * [1024, bn_op_max_bits(op)].  Every operation covers [1024, 262144] (the
+ * paper's 2^11..2^18 sweep, PAPER.md:919 and Tables 1-2, plus 2^10), one
+ * instance (or several) per CTA: 262144 bits is the largest size whose exact
+ * NTT product fits one CTA's shared memory.  bn_add and bn_mul_ntt go on to
+ * 2^19 and 2^20 bits with one instance per thread-block cluster of 2 / 4
+ * CTAs (carries and NTT exchanges through distributed shared memory,
+ * DESIGN.md §7d); bn_mul_wide_ntt stops at 2^17.  Other sizes -> BN_ESIZE.
  *
  * POINTERS: a, b, out are DEVICE pointers on the current CUDA device, 16-byte
  * aligned.  out may equal a or b exactly (in-place); a partial overlap is
@@ -47,7 +51,7 @@ typedef struct CUstream_st *bn_stream_t; /* == cudaStream_t */
 typedef enum {
     BN_OK = 0,
     BN_EINVAL = 1, /* NULL pointer, limb_bits not 32/64, n_limbs == 0, bad op */
-    BN_ESIZE = 2,  /* n_limbs*limb_bits not a power of two in [1024, 262144] */
+    BN_ESIZE = 2,  /* n_limbs*limb_bits not a power of two in [1024, bn_op_max_bits(op)] */
     BN_EALIGN = 3, /* a, b or out not 16-byte aligned */
     BN_EALIAS = 4, /* out partially overlaps a or b (exact equality allowed) */
     BN_ECUDA = 5,  /* CUDA launch / configuration / copy failure */
@@ -170,7 +174,8 @@ bn_status bn_run_host(const int *ops, void *const *outs, int n_ops, const void *
                       const void *b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
 
 /* ---- introspection ------------------------------------------------------ */
-uint32_t bn_max_bits(void);                /* 262144 */
+uint32_t bn_max_bits(void);                /* 1048576: the largest size any op accepts */
+uint32_t bn_op_max_bits(int op);           /* per BN_OP_* code; 0 for an unknown op */
 uint32_t bn_min_bits(void);                /* 1024 */
 int bn_cuda_error(void);                   /* last cudaError_t seen by this thread */
 const char *bn_status_string(bn_status s); /* static string */

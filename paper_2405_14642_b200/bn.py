@@ -24,7 +24,7 @@ _LIB_PATH = os.environ.get("BN_LIB_PATH") or os.path.join(_HERE, "libbn.so")
 _lock = threading.Lock()
 _lib = None
 
-SUPPORTED_BITS = tuple(1 << k for k in range(10, 19))
+SUPPORTED_BITS = tuple(1 << k for k in range(10, 19))  # every op; add / mul_ntt go to 2^20
 
 _STATUS = {0: "BN_OK", 1: "BN_EINVAL", 2: "BN_ESIZE", 3: "BN_EALIGN", 4: "BN_EALIAS",
            5: "BN_ECUDA", 6: "BN_ENODEV"}
@@ -70,6 +70,7 @@ def load():
                 "bn_prepare": ([i32], i32),
                 "bn_run_host": ([ctypes.POINTER(i32), ctypes.POINTER(vp), i32, vp, vp, u64, u32, u32], i32),
                 "bn_max_bits": ([], u32),
+                "bn_op_max_bits": ([i32], u32),
                 "bn_min_bits": ([], u32),
                 "bn_cuda_error": ([], i32),
                 "bn_status_string": ([i32], ctypes.c_char_p),
@@ -89,8 +90,11 @@ def load():
     return _lib
 
 
-def max_bits() -> int:
-    return int(load().bn_max_bits())
+def max_bits(op: str = None) -> int:
+    """Largest supported size in bits (of `op`, else of any op)."""
+    if op is None:
+        return int(load().bn_max_bits())
+    return int(load().bn_op_max_bits(OPS[op]))
 
 
 def _limb_bits(t: torch.Tensor) -> int:

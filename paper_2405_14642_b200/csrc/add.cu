@@ -14,8 +14,12 @@
 // (grid-stride over instance groups) so small sizes amortise launch and
 // tail effects.  HBM-bound: 3 * bits / 8 algorithmic bytes per instance
 // (PAPER.md:929).
+#include <cooperative_groups.h>
+
 #include "bn_common.cuh"
 #include "bn_kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace bn {
 
@@ -93,6 +97,61 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
   }
 }
 
+// Sizes beyond one CTA (2^19, 2^20 bits): one instance per
+// thread-block cluster of CR = M / 8192 CTAs (2 or 4), CTA rank r holding
+// limbs [r M/CR, (r+1) M/CR), 1024 threads x 8 limbs.  The carry scan runs
+// across the cluster (cluster_carry_scan: the CTA aggregates travel through
+// DSMEM) — the hierarchical scan of PAPER.md:289-292 with one more level,
+// instead of the single-pass decoupled look-back over global memory the
+// paper cites.
+template <int LOGM>
+__global__ void __launch_bounds__(1024, 1)
+    add_cluster_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
+                       const uint32_t* __restrict__ b, uint64_t n_inst) {
+  constexpr int M = 1 << LOGM, L = 8, CR = M / (1024 * L);
+  __shared__ uint32_t agg[32];
+  __shared__ uint32_t cta_agg[2 * CR];
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  const uint64_t n_cl = gridDim.x / CR;
+  int parity = 0;
+  for (uint64_t inst = blockIdx.x / CR; inst < n_inst; inst += n_cl, parity ^= 1) {
+    const uint64_t off = inst * (uint64_t)M + (uint64_t)rank * (M / CR) + (uint64_t)threadIdx.x * L;
+    uint32_t x[L], y[L], r[L], g, p;
+    load_limbs<L>(x, a + off);
+    load_limbs<L>(y, b + off);
+    chunk_sum<L>(x, y, r, g, p);
+    if (rank == CR - 1 && threadIdx.x == 1023) g = p = 0;  // the instance's top carry-out is dropped
+    const uint32_t cin = cluster_carry_scan<CR>(g, p, agg, cta_agg, parity, cl);
+    chunk_apply<L>(x, r, cin);
+    store_limbs<L>(out + off, r);
+  }
+}
+
+template <int LOGM>
+static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                        cudaStream_t st, int n_sm) {
+  constexpr int CR = (1 << LOGM) / 8192;
+  const uint64_t max_cl = (uint64_t)(n_sm / CR) * 2;
+  uint64_t n_cl = n_inst < max_cl ? n_inst : max_cl;
+  n_cl = cap_grid((unsigned)n_cl);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_cl * CR));
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CR;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, add_cluster_kernel<LOGM>, out, a, b, n_inst);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 template <int LOGM>
 static cudaError_t launch_add6_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                  cudaStream_t st, int n_sm) {
@@ -123,6 +182,8 @@ static cudaError_t launch_add_t(uint32_t* out, const uint32_t* a, const uint32_t
 cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                        cudaStream_t st, int n_sm) {
   switch (logm) {
+    case 14: return launch_add_cluster_t<14>(out, a, b, n_inst, st, n_sm);
+    case 15: return launch_add_cluster_t<15>(out, a, b, n_inst, st, n_sm);
     case 5: return launch_add_t<5>(out, a, b, n_inst, st, n_sm);
     case 6: return launch_add_t<6>(out, a, b, n_inst, st, n_sm);
     case 7: return launch_add_t<7>(out, a, b, n_inst, st, n_sm);

@@ -21,13 +21,27 @@ namespace {
 thread_local int tls_cuda_err = 0;
 
 constexpr int kMaxDev = 64;
-constexpr uint32_t kMinBits = 1024, kMaxBits = 262144;
+constexpr uint32_t kMinBits = 1024, kMaxBits = 1048576;
 
-// The three NTT primes, p0 < p1 < p2 < 2^30, each p = k 2^e + 1 with e >= 14
-// (so every N = 2^6 .. 2^14 has a primitive N-th root), product 2^89.99 >
-// 2^77 >= the largest coefficient m (2^32-1)^2 at m = 8192 (DESIGN.md,
-// reading R10).  Verified prime at start-up by a deterministic Miller-Rabin.
-constexpr uint32_t kPrimes[bn::kNumPrimes] = {1073479681u, 1073643521u, 1073692673u};
+// Largest log2(bits) per operation: 2^18 fits one CTA (the paper's range);
+// add and the NTT product go to 2^20 on thread-block clusters (SURVEY
+// §8(f) #4); the wide NTT product stops at 2^17 (shared memory).
+int op_max_lb(int op) {
+  switch (op) {
+    case BN_OP_ADD: case BN_OP_MUL_NTT: return 20;
+    case BN_OP_MUL_WIDE_NTT: return 17;
+    case BN_OP_MUL_CLASSICAL: case BN_OP_ADD6: case BN_OP_POLY_CLASSICAL: case BN_OP_POLY_NTT:
+    case BN_OP_MUL_WIDE_CLASSICAL: return 18;
+    default: return -1;
+  }
+}
+
+// The three NTT primes, p0 < p1 < p2 < 2^30, each p = k 2^17 + 1 (the three
+// largest such primes below 2^30, so every N = 2^6 .. 2^17 has a primitive
+// N-th root), product 2^89.99 > 2^79 >= the largest coefficient
+// m (2^32-1)^2 at m = 32768 (1M-bit operands, reading R10).
+// Verified prime at start-up by a deterministic Miller-Rabin.
+constexpr uint32_t kPrimes[bn::kNumPrimes] = {1070727169u, 1071513601u, 1073479681u};
 
 // ---------------------------------------------------------------- number theory (host)
 uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((unsigned __int128)a * b % m); }
@@ -227,13 +241,13 @@ int ilog2_exact(uint64_t v) {
 }
 
 // validation shared by the three ops; returns log2(u32 limbs)
-bn_status validate(const void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
+bn_status validate(int op, const void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
                    uint32_t limb_bits, int* logm) {
   if (limb_bits != 32 && limb_bits != 64) return BN_EINVAL;
   if (n_limbs == 0) return BN_EINVAL;
   const uint64_t bits = (uint64_t)n_limbs * limb_bits;
   const int lb = ilog2_exact(bits);
-  if (lb < 10 || lb > 18) return BN_ESIZE;
+  if (lb < 10 || lb > op_max_lb(op)) return BN_ESIZE;
   *logm = lb - 5;
   if (n_inst == 0) return BN_OK;
   if (!out || !a || !b) return BN_EINVAL;
@@ -250,7 +264,7 @@ bn_status validate(const void* out, const void* a, const void* b, uint64_t n_ins
 bn_status run_op(int op, void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
                  uint32_t limb_bits, cudaStream_t st) {
   int logm = 0;
-  bn_status s = validate(out, a, b, n_inst, n_limbs, limb_bits, &logm);
+  bn_status s = validate(op, out, a, b, n_inst, n_limbs, limb_bits, &logm);
   if (s != BN_OK || n_inst == 0) return s;
   DevState* d = nullptr;
   s = current_device(&d);
@@ -275,11 +289,10 @@ bn_status run_wide(int op, void* out, const void* a, const void* b, uint64_t n_i
                    uint32_t limb_bits, cudaStream_t st) {
   int logm = 0;
   // operand checks (out is checked below against its doubled size)
-  bn_status s = validate(a, a, a, n_inst, n_limbs, limb_bits, &logm);
+  bn_status s = validate(op, a, a, a, n_inst, n_limbs, limb_bits, &logm);
   if (s != BN_OK) return s;
   if (n_inst && !b) return BN_EINVAL;
   if (n_inst && ((uintptr_t)b & 15)) return BN_EALIGN;
-  if (op == BN_OP_MUL_WIDE_NTT && logm > 12) return BN_ESIZE;
   if (n_inst == 0) return BN_OK;
   if (!out) return BN_EINVAL;
   if ((uintptr_t)out & 15) return BN_EALIGN;
@@ -320,7 +333,7 @@ bn_status launch_poly(int op, int logm, uint32_t* o, const uint32_t* x, const ui
 bn_status run_poly(int op, void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs,
                    uint32_t limb_bits, void* ws, uint64_t ws_bytes, cudaStream_t st) {
   int logm = 0;
-  bn_status s = validate(out, a, b, n_inst, n_limbs, limb_bits, &logm);
+  bn_status s = validate(op, out, a, b, n_inst, n_limbs, limb_bits, &logm);
   if (s != BN_OK || n_inst == 0) return s;
   DevState* d = nullptr;
   s = current_device(&d);
@@ -378,7 +391,7 @@ bn_status bn_mul_wide_ntt(void* out, const void* a, const void* b, uint64_t n_in
 uint64_t bn_poly_workspace_bytes(int op, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits) {
   if (!is_poly(op)) return 0;
   int logm = 0;
-  if (validate((void*)16, (void*)16, (void*)16, 0, n_limbs, limb_bits, &logm) != BN_OK) return 0;
+  if (validate(op, (void*)16, (void*)16, (void*)16, 0, n_limbs, limb_bits, &logm) != BN_OK) return 0;
   if (n_inst == 0) return 0;
   DevState* d = nullptr;
   if (current_device(&d) != BN_OK) return 0;
@@ -409,14 +422,16 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   if (n_ops <= 0 || !ops || !outs) return BN_EINVAL;
   int logm = 0;
   // validate sizes with dummy aligned device pointers (host buffers may alias-check only)
-  bn_status s = validate((void*)16, (void*)16, (void*)16, 0, n_limbs, limb_bits, &logm);
-  if (s != BN_OK) return s;
+  for (int i = 0; i < n_ops; i++) {
+    if (ops[i] < BN_OP_ADD || ops[i] > BN_OP_POLY_NTT) return BN_EINVAL;
+    bn_status s = validate(ops[i], (void*)16, (void*)16, (void*)16, 0, n_limbs, limb_bits, &logm);
+    if (s != BN_OK) return s;
+  }
   if (n_inst == 0) return BN_OK;
   if (!a || !b) return BN_EINVAL;
-  for (int i = 0; i < n_ops; i++) {
+  for (int i = 0; i < n_ops; i++)
     if (!outs[i]) return BN_EINVAL;
-    if (ops[i] < BN_OP_ADD || ops[i] > BN_OP_POLY_NTT) return BN_EINVAL;
-  }
+  bn_status s;
   DevState* d = nullptr;
   s = current_device(&d);
   if (s != BN_OK) return s;
@@ -501,7 +516,7 @@ const char* bn_status_string(bn_status s) {
   switch (s) {
     case BN_OK: return "BN_OK";
     case BN_EINVAL: return "BN_EINVAL: invalid argument";
-    case BN_ESIZE: return "BN_ESIZE: bits must be a power of two in [1024, 262144]";
+    case BN_ESIZE: return "BN_ESIZE: bits must be a power of two in [1024, bn_op_max_bits(op)]";
     case BN_EALIGN: return "BN_EALIGN: buffers must be 16-byte aligned";
     case BN_EALIAS: return "BN_EALIAS: out partially overlaps an input";
     case BN_ECUDA: return "BN_ECUDA: CUDA error (see bn_cuda_error)";
@@ -510,11 +525,14 @@ const char* bn_status_string(bn_status s) {
   return "unknown bn_status";
 }
 
+uint32_t bn_op_max_bits(int op) {
+  const int lb = op_max_lb(op);
+  return lb < 0 ? 0u : (1u << lb);
+}
+
 uint32_t bn_launches_per_call(int op, uint32_t bits) {
-  if (op < BN_OP_ADD || op > BN_OP_MUL_WIDE_NTT) return 0;
   const int lb = ilog2_exact(bits);
-  if (lb < 10 || lb > 18) return 0;
-  if (op == BN_OP_MUL_WIDE_NTT && lb > 17) return 0;
+  if (lb < 10 || lb > op_max_lb(op)) return 0;
   return 1;
 }
 
@@ -526,7 +544,7 @@ void bn_ntt_primes(uint32_t p[3]) {
 
 bn_status bn_debug_ntt_forward(uint32_t* x, uint64_t n_inst, uint32_t lg_n, int prime, uint32_t* omega_out,
                                bn_stream_t stream) {
-  if ((int)lg_n < bn::kMinLogN || (int)lg_n > bn::kMaxLogN || prime < 0 || prime >= bn::kNumPrimes)
+  if ((int)lg_n < bn::kMinLogN || (int)lg_n > bn::kMaxLogNOneCta || prime < 0 || prime >= bn::kNumPrimes)
     return BN_EINVAL;
   DevState* d = nullptr;
   bn_status s = current_device(&d);

@@ -196,6 +196,61 @@ BN_DEV uint32_t carry_scan(uint32_t g, uint32_t p, uint32_t* agg) {
   }
 }
 
+// ------------------------------------------------------- DSMEM primitives
+// 32-bit shared::cluster addressing (half the registers of generic pointers):
+// the address of `p` (this CTA's shared memory) in CTA `rank` of the cluster.
+BN_DEV uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+BN_DEV uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+BN_DEV void st_cluster(uint32_t caddr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(caddr), "r"(v) : "memory");
+}
+
+// ------------------------------------------------------- cluster carry scan
+// One instance spread over the CR CTAs of a thread-block cluster (sizes
+// beyond one CTA): CTA rank r holds the r-th contiguous
+// slice of the limbs, every CTA has 1024 threads.  Three levels of the same
+// carry operator (hierarchical as in PAPER.md:289-292):
+// lanes (ballot-add), warps (ballot-add over the 32 warp aggregates), CTAs
+// (each CTA's aggregate is written into every CTA's shared memory through
+// DSMEM, then folded sequentially: CR <= 16).  The carry into the CTA enters
+// the warp-level ballot-add as its initial carry.  cta_agg: CR words of
+// shared memory per buffer, double-buffered by `parity` so consecutive
+// instances need one cluster barrier each.  Every thread of every CTA of the
+// cluster must call it.
+template <int CR, class Cluster>
+BN_DEV uint32_t cluster_carry_scan(uint32_t g, uint32_t p, uint32_t* agg, uint32_t* cta_agg, int parity,
+                                   Cluster& cl) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t G = __ballot_sync(0xFFFFFFFFu, g);
+  const uint32_t P = __ballot_sync(0xFFFFFFFFu, p);
+  const uint32_t X = G | P;
+  if (lane == 0) agg[warp] = (uint32_t)(((uint64_t)X + G) >> 32) | ((P == 0xFFFFFFFFu) << 1);
+  __syncthreads();
+  const uint32_t a = agg[lane];  // blockDim.x == 1024: 32 warp aggregates
+  const uint32_t G2 = __ballot_sync(0xFFFFFFFFu, a & 1u);
+  const uint32_t P2 = __ballot_sync(0xFFFFFFFFu, (a >> 1) & 1u);
+  const uint32_t X2 = G2 | P2;
+  const unsigned rank = cl.block_rank();
+  uint32_t* buf = cta_agg + parity * CR;
+  if (threadIdx.x < CR) {
+    // this CTA's aggregate into slot `rank` of CTA threadIdx.x (DSMEM)
+    const uint32_t v = (uint32_t)(((uint64_t)X2 + G2) >> 32) | ((P2 == 0xFFFFFFFFu) << 1);
+    st_cluster(mapa_rank(smem_addr(buf + rank), threadIdx.x), v);
+  }
+  cl.sync();
+  uint32_t c_cta = 0;
+  for (unsigned r = 0; r < rank; r++) {
+    const uint32_t v = buf[r];
+    c_cta = (v & 1u) | ((v >> 1) & c_cta);
+  }
+  const uint32_t c0 = (((X2 + G2 + c_cta) ^ X2 ^ G2) >> warp) & 1u;
+  return (((X + G + c0) ^ X ^ G) >> lane) & 1u;
+}
+
 // r = x + y over an instance whose L*TPI limbs are spread over TPI
 // consecutive threads (thread k holds limbs [k*L, (k+1)*L)); valid == false
 // threads contribute kill and their result is garbage (not stored).

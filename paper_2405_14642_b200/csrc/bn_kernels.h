@@ -8,11 +8,12 @@ namespace bn {
 
 constexpr int kNumPrimes = 3;
 constexpr int kMinLogN = 6;   // N = 2m, m = 32 limbs (1024 bits)
-constexpr int kMaxLogN = 14;  // m = 8192 limbs (262144 bits)
+constexpr int kMaxLogN = 16;  // m = 32768 limbs (1048576 bits; N > 2^14 runs on a CTA cluster)
+constexpr int kMaxLogNOneCta = 14;  // m = 8192 limbs (262144 bits): one instance per CTA
 
 // Per-prime constants of the exact NTT product (host-computed in bn_api.cu).
 struct PrimeConst {
-  uint32_t p;      // prime, 2^29 < p < 2^30, p = k 2^e + 1 with e >= 14
+  uint32_t p;      // prime, 2^29 < p < 2^30, p = k 2^17 + 1
   uint32_t p2;     // 2p
   uint32_t pinv;   // -p^-1 mod 2^32 (Montgomery)
   uint32_t one_sh; // floor(2^32 / p): Shoup constant of w = 1 (input reduction)

@@ -25,8 +25,12 @@
 // Per thread, then, 8 consecutive coefficients are CRT'd and aggregated into
 // 8 low words + 2 overflow words (< 2^46), published into L/H exactly like
 // the classical kernel (reading R8) and resolved by the §2 scan-add.
+#include <cooperative_groups.h>
+
 #include "bn_common.cuh"
 #include "bn_kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace bn {
 
@@ -560,6 +564,222 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
   }
 }
 
+// ------------------------------------------------------------ beyond one CTA
+// N = 2^15, 2^16 (512K / 1M-bit operands): one instance per
+// thread-block cluster of CR = N / 16384 CTAs of 1024 threads x 16 register
+// elements; global thread gt = rank * 1024 + tid runs exactly the register
+// passes of the one-CTA kernel (the passes only see gt).  Exchanges go
+// through distributed shared memory: the writer stores each element into the
+// CTA (and slot e * 1024 + tid) of the thread that reads it in the next
+// layout, then a cluster barrier, then purely local, conflict-free reads.
+// With LOGN - 4(P+1) low bits per pass, the CTA-rank bits of gt land on the
+// top index bits in every layout but pass 0's, so only the pass 0 <-> 1
+// exchanges move data between CTAs.  Residues are stored with consecutive
+// ownership (CTA r owns coefficients [r M/CR, (r+1) M/CR)), so the CRT,
+// aggregation and L / H publish are local except one 8-word H spill per CTA,
+// and the resolve is the cluster-wide carry scan.
+template <int LOGN>
+struct NttClCfg {
+  static constexpr int N = 1 << LOGN, M = N / 2, T = 1024;
+  static constexpr int CR = N / (T * 16);
+  static constexpr int PL = T * 16;   // words of one exchange plane per CTA
+  static constexpr int MS = M / CR;   // coefficients / limbs owned by a CTA
+  static constexpr int SMEM_WORDS = 2 * PL + 3 * MS + 32 + 2 * CR;
+  static_assert(CR >= 2 && MS == 8 * T, "cluster layout");
+};
+
+template <int LO>
+BN_DEV int unlay_t(int u) { return (u & ((1 << LO) - 1)) | ((u >> (LO + 4)) << LO); }
+
+template <int LOGN, int LO_FROM, int LO_TO, int NV, class Cluster>
+BN_DEV void xchg_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, Cluster& cl) {
+  using C = NttClCfg<LOGN>;
+  cl.sync();  // every reader of every CTA's planes is done
+  const uint32_t x0 = smem_addr(X0);
+#pragma unroll
+  for (int e = 0; e < 16; e++) {
+    const int u = lay<LO_FROM>(gt, e);
+    const int gto = unlay_t<LO_TO>(u);
+    const int eto = (u >> LO_TO) & 15;
+    const uint32_t dst = mapa_rank(x0 + 4 * (eto * C::T + (gto & (C::T - 1))), gto / C::T);
+#pragma unroll
+    for (int v = 0; v < NV; v++) st_cluster(dst + 4 * v * C::PL, x[v][e]);
+  }
+  cl.sync();
+#pragma unroll
+  for (int v = 0; v < NV; v++)
+#pragma unroll
+    for (int e = 0; e < 16; e++) x[v][e] = X0[v * C::PL + e * C::T + threadIdx.x];
+}
+
+template <int LOGN, int NV, class Cluster>
+BN_DEV void fwd_all_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, const uint2* tw, uint32_t p, uint32_t p2,
+                       Cluster& cl) {
+  fwd_pass<LOGN, 0, true, NV>(x, gt, tw, p, p2);
+  xchg_cl<LOGN, PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, NV>(x, X0, gt, cl);
+  fwd_pass<LOGN, 1, true, NV>(x, gt, tw, p, p2);
+  xchg_cl<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, NV>(x, X0, gt, cl);
+  fwd_pass<LOGN, 2, true, NV>(x, gt, tw, p, p2);
+  xchg_cl<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, NV>(x, X0, gt, cl);
+  fwd_pass<LOGN, 3, true, NV>(x, gt, tw, p, p2);
+}
+
+template <int LOGN, class Cluster>
+BN_DEV void inv_all_cl(uint32_t (&x1)[16], uint32_t* X0, int gt, const uint2* tw, uint32_t p, uint32_t p2,
+                       Cluster& cl) {
+  uint32_t(&x)[1][16] = reinterpret_cast<uint32_t(&)[1][16]>(x1);
+  inv_pass<LOGN, 3>(x1, gt, tw, p, p2);
+  xchg_cl<LOGN, PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, 1>(x, X0, gt, cl);
+  inv_pass<LOGN, 2>(x1, gt, tw, p, p2);
+  xchg_cl<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, 1>(x, X0, gt, cl);
+  inv_pass<LOGN, 1>(x1, gt, tw, p, p2);
+  xchg_cl<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, 1>(x, X0, gt, cl);
+  inv_pass<LOGN, 0>(x1, gt, tw, p, p2);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1024, 1)
+    mul_ntt_cluster_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                           const uint2* __restrict__ tw) {
+  using C = NttClCfg<LOGN>;
+  constexpr int N = C::N, M = C::M, MS = C::MS;
+  extern __shared__ __align__(16) uint32_t sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const int gt = rank * C::T + tid;
+  uint32_t* X0 = sm;                  // plane 0 | plane 1
+  uint32_t* Res = sm + 2 * C::PL;     // 3 x MS, consecutive ownership
+  uint32_t* agg = Res + 3 * MS;       // 32
+  uint32_t* cta_agg = agg + 32;       // 2 CR
+  const uint64_t n_cl = gridDim.x / C::CR;
+  int parity = 0;
+  for (uint64_t inst = blockIdx.x / C::CR; inst < n_inst; inst += n_cl, parity ^= 1) {
+    const uint32_t* ai = a + inst * M;
+    const uint32_t* bi = b + inst * M;
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xab[2][16];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        xab[0][e] = red2(red2(__ldg(ai + gt + e * (N / 16)), p2), p2);
+        xab[1][e] = red2(red2(__ldg(bi + gt + e * (N / 16)), p2), p2);
+      }
+#pragma unroll
+      for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
+      fwd_all_cl<LOGN, 2>(xab, X0, gt, twf, p, p2, cl);
+      uint32_t x[16];
+#pragma unroll
+      for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[1][e], p, pinv);
+      inv_all_cl<LOGN>(x, X0, gt, twi, p, p2, cl);
+      // coefficient k = gt + e N/16 (e < 8) -> its owner's residue array
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const int k = gt + e * (N / 16);
+        st_cluster(mapa_rank(smem_addr(Res + j * MS + (k & (MS - 1))), k / MS), x[e]);
+      }
+    }
+    cl.sync();  // residues in place; every plane read is done
+
+    // N-5 / N-6 on this CTA's consecutive coefficients [rank MS + 8 tid, +8)
+    {
+      const CrtConst& k = c_crt[LOGN];
+      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+      uint32_t y0[8], y1[8], y2[8];
+      lds_limbs<8>(y0, Res + 0 * MS + 8 * tid);
+      lds_limbs<8>(y1, Res + 1 * MS + 8 * tid);
+      lds_limbs<8>(y2, Res + 2 * MS + 8 * tid);
+      uint32_t lows[8], hs[8];
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+        const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+        const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+        const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+        const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+        const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+        const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+        const uint32_t d = red2(b2v + c2v, 2 * p2);
+        const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+        const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+        const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+        const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
+        add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
+        lows[q] = a0;
+        a0 = a1;
+        a1 = a2;
+        a2 = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      // L = plane 0 [0, MS), H = plane 1 [0, MS) (planes are dead)
+      uint32_t* L = X0;
+      uint32_t* H = X0 + C::PL;
+      sts_limbs<8>(L + 8 * tid, lows);
+      if (tid < C::T - 1) {
+        sts_limbs<8>(H + 8 * tid + 8, hs);
+      } else {
+        // the CTA's top chunk spills into the next CTA's H[0, 8); the
+        // instance's top chunk wraps to zero CTA 0's H[0, 8)
+        if (rank == C::CR - 1) {
+#pragma unroll
+          for (int q = 0; q < 8; q++) hs[q] = 0;
+        }
+        const uint32_t dst = mapa_rank(smem_addr(H), (rank + 1) % C::CR);
+#pragma unroll
+        for (int q = 0; q < 8; q++) st_cluster(dst + 4 * q, hs[q]);
+      }
+    }
+    cl.sync();
+    // N-7: R = L + H across the cluster, store
+    {
+      uint32_t xl[8], yh[8], r[8], g, pp;
+      lds_limbs<8>(xl, X0 + 8 * tid);
+      lds_limbs<8>(yh, X0 + C::PL + 8 * tid);
+      chunk_sum<8>(xl, yh, r, g, pp);
+      const uint32_t cin = cluster_carry_scan<C::CR>(g, pp, agg, cta_agg, parity, cl);
+      chunk_apply<8>(xl, r, cin);
+      store_limbs<8>(out + inst * M + (uint64_t)rank * MS + 8 * tid, r);
+    }
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_ntt_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                        const NttTables& tb, cudaStream_t st, int n_sm) {
+  using C = NttClCfg<LOGN>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(mul_ntt_cluster_kernel<LOGN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CR;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(C::CR);
+  int max_cl = 0;
+  e = cudaOccupancyMaxActiveClusters(&max_cl, mul_ntt_cluster_kernel<LOGN>, &cfg);
+  if (e != cudaSuccess) return e;
+  if (max_cl < 1) return cudaErrorInvalidConfiguration;
+  uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
+  n_cl = cap_grid((unsigned)n_cl);
+  cfg.gridDim = dim3((unsigned)(n_cl * C::CR));
+  e = cudaLaunchKernelEx(&cfg, mul_ntt_cluster_kernel<LOGN>, out, a, b, n_inst, tb.tw);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ full product
 // Wide (untruncated) product: out[k] = a[k] * b[k] as 2m
 // limbs.  The N = 2m point transform already yields every coefficient
@@ -809,6 +1029,8 @@ static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const N
 cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                            uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm) {
   switch (logm + 1) {
+    case 15: return launch_ntt_cluster_t<15>(out, a, b, n_inst, tb, st, n_sm);
+    case 16: return launch_ntt_cluster_t<16>(out, a, b, n_inst, tb, st, n_sm);
     case 6: return launch_ntt_t<6>(out, a, b, n_inst, tb, st, n_sm);
     case 7: return launch_ntt_t<7>(out, a, b, n_inst, tb, st, n_sm);
     case 8: return launch_ntt_t<8>(out, a, b, n_inst, tb, st, n_sm);

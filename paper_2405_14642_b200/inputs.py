@@ -65,7 +65,10 @@ def _hash_grid(seed: int, operand: int, inst0: int, n_inst: int, m: int, device)
     """u32 hash (as int64 in [0, 2^32)) for every (instance, limb)."""
     inst = torch.arange(inst0, inst0 + n_inst, dtype=torch.int64, device=device).view(-1, 1)
     limb = torch.arange(m, dtype=torch.int64, device=device).view(1, -1)
-    ctr = (inst << 14) | limb  # m <= 8192 < 2^14
+    if m <= 8192:
+        ctr = (inst << 14) | limb  # m <= 8192 < 2^14
+    else:  # cluster sizes: m <= 32768 < 2^16, separate counter domain (bit 62)
+        ctr = (inst << 16) | limb | (1 << 62)
     return _lsr(splitmix64(ctr ^ _key(seed, operand)), 32)
 
 
@@ -112,8 +115,8 @@ def make_operands(n_inst: int, m: int, seed: int = 1, cls: str = "U", inst0: int
     sharding of the instance range."""
     if cls not in CLASSES:
         raise ValueError("unknown input class %r (one of %s)" % (cls, CLASSES))
-    if m < 1 or m > 8192:
-        raise ValueError("m must be in [1, 8192]")
+    if m < 1 or m > 32768:
+        raise ValueError("m must be in [1, 32768]")
     if n_inst == 0:
         z = torch.zeros((0, m), dtype=torch.int32, device=device)
         return z, z.clone()

@@ -75,7 +75,9 @@ def test_validation_before_launch(lib, op):
     assert _call(lib, op, O, A, B, 4, 0, 32) == 1          # n_limbs == 0
     assert _call(lib, op, O, A, B, 4, 48, 32) == 2         # 1536 bits: not a power of two
     assert _call(lib, op, O, A, B, 4, 16, 32) == 2         # 512 bits: below 1024
-    assert _call(lib, op, O, A, B, 4, 16384, 32) == 2      # 2^19 bits: above one CTA
+    big = 2 if op in ("bn_mul_classical", "bn_add6") else 0
+    assert _call(lib, op, O, A, B, 0, 16384, 32) == big    # 2^19 bits: cluster sizes for add / NTT
+    assert _call(lib, op, O, A, B, 4, 65536, 32) == 2      # 2^21 bits: beyond every op
     assert _call(lib, op, O, A, B, 0, 32, 32) == 0         # n_inst == 0: OK, no launch
     assert _call(lib, op, O, A + 4, B, 4, 32, 32) == 3     # misaligned a
     assert _call(lib, op, O + 8, A, B, 4, 32, 32) == 3     # misaligned out
@@ -88,11 +90,14 @@ def test_u64_size_rules(lib):
     A, B, O = 0x10000, 0x200000, 0x4000000
     # 4096 u64 limbs = 262144 bits: valid size; it would launch, so only check n_inst=0
     assert _call(lib, "bn_add", O, A, B, 0, 4096, 64) == 0
-    assert _call(lib, "bn_add", O, A, B, 0, 8192, 64) == 2
+    assert _call(lib, "bn_add", O, A, B, 0, 8192, 64) == 0     # 2^19 bits: cluster size
+    assert _call(lib, "bn_add", O, A, B, 0, 32768, 64) == 2
 
 
 def test_introspection(lib):
-    assert lib.bn_max_bits() == 262144 and lib.bn_min_bits() == 1024
+    assert lib.bn_max_bits() == 1 << 20 and lib.bn_min_bits() == 1024
+    assert [lib.bn_op_max_bits(op) for op in range(8)] == \
+        [1 << 20, 1 << 18, 1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 18, 1 << 17]
     assert lib.bn_status_string(3).startswith(b"BN_EALIGN")
     for op in range(6):
         assert lib.bn_launches_per_call(op, 4096) == 1
@@ -100,7 +105,7 @@ def test_introspection(lib):
     arr = (ctypes.c_uint32 * 3)()
     lib.bn_ntt_primes(arr)
     ps = list(arr)
-    assert ps == sorted(ps) and all(2**29 < p < 2**30 and (p - 1) % (1 << 14) == 0 for p in ps)
+    assert ps == sorted(ps) and all(2**29 < p < 2**30 and (p - 1) % (1 << 17) == 0 for p in ps)
 
 
 def test_binding_refuses_cpu_tensors(lib):
@@ -132,7 +137,7 @@ def test_poly_validation_before_launch(lib, op):
     call = lambda o, a, b, n, limbs, bits: f(vp(o), vp(a), vp(b), n, limbs, bits, vp(W), 1 << 20, None)
     assert call(O, A, B, 4, 32, 7) == 1
     assert call(O, A, B, 4, 48, 32) == 2
-    assert call(O, A, B, 4, 16384, 32) == 2
+    assert call(O, A, B, 4, 16384, 32) == 2                 # Poly: one CTA only
     assert call(O, A, B, 0, 32, 32) == 0
     assert call(O, A + 4, B, 4, 32, 32) == 3
     assert call(A + 16, A, B, 4, 32, 32) == 4

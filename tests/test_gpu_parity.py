@@ -431,3 +431,66 @@ def test_wide_full_size_4096():
     idx = torch.tensor([0, 12345, n - 1], device=DEV)
     want = O.mul_full_rows(inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx]))
     assert np.array_equal(inputs.to_numpy_u32(wc[idx]), want)
+
+
+# ------------------------- beyond one CTA: thread-block clusters (§8(f) #4)
+
+CLUSTER_SIZES = [1 << 19, 1 << 20]
+
+
+@pytest.mark.parametrize("cls", ["U", "ONES", "RIPPLE", "RUNS", "MIX"])
+@pytest.mark.parametrize("bits", CLUSTER_SIZES)
+def test_parity_cluster_sizes(bits, cls):
+    """bn_add and bn_mul_ntt at 512K / 1M bits (one instance per cluster of
+    2 / 4 CTAs) vs the oracle, bit-exact; carries cross CTA boundaries
+    (RIPPLE: through every thread, warp and CTA)."""
+    m = bits // 32
+    n = 3
+    a, b = inputs.make_operands(n, m, seed=bits % 1000 + len(cls), cls=cls)
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    da, db = a.to(DEV), b.to(DEV)
+    got = inputs.to_numpy_u32(bn.add(da, db))
+    bad = _first_bad(got, O.add(an, bnp))
+    assert bad is None, "add %d %s: %s" % (bits, cls, bad)
+    got = inputs.to_numpy_u32(bn.mul_ntt(da, db))
+    bad = _first_bad(got, O.mul(an, bnp, nthreads=8))
+    assert bad is None, "mul_ntt %d %s: %s" % (bits, cls, bad)
+
+
+@pytest.mark.parametrize("bits", CLUSTER_SIZES)
+def test_cluster_full_batch_closed_forms(bits):
+    """Paper batch (2^32 bits per operand) at 512K / 1M bits: all-ones closed
+    forms on every instance, grid-stride over clusters."""
+    m = bits // 32
+    n = (1 << 32) // bits
+    ones, _ = inputs.make_operands(n, m, seed=1, cls="ONES", device=DEV)
+    _, rip = inputs.make_operands(n, m, seed=1, cls="RIPPLE", device=DEV)
+    one = torch.zeros((m,), dtype=torch.int32, device=DEV)
+    one[0] = 1
+    assert torch.equal(bn.mul_ntt(ones, ones), one.expand(n, m))
+    assert not bn.add(ones, rip).any()
+    assert torch.equal(bn.mul_ntt(ones, rip), ones)
+    s = bn.add(ones, ones)
+    want = torch.full((m,), -1, dtype=torch.int32, device=DEV)
+    want[0] = -2
+    assert torch.equal(s, want.expand(n, m))
+
+
+@pytest.mark.parametrize("cap", [2, 4])
+def test_cluster_grid_cap(cap):
+    """Clusters that each run several instances (cluster-count cap) give the
+    same results as the oracle (R20); exercises the double-buffered CTA
+    aggregates of the cluster carry scan."""
+    bits = 1 << 19
+    m = bits // 32
+    a, b = inputs.make_operands(7, m, seed=cap, cls="MIX")
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    da, db = a.to(DEV), b.to(DEV)
+    bn.debug_set_grid_cap(cap)
+    try:
+        ga = inputs.to_numpy_u32(bn.add(da, db))
+        gm = inputs.to_numpy_u32(bn.mul_ntt(da, db))
+    finally:
+        bn.debug_set_grid_cap(0)
+    assert _first_bad(ga, O.add(an, bnp)) is None
+    assert _first_bad(gm, O.mul(an, bnp, nthreads=8)) is None
