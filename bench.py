@@ -425,8 +425,9 @@ def load_traffic(kernel: str, bits: int):
 
 
 def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barrier):
-    """Per-(op, size) lines over 1K..256K bits, paper batch 2^32 bits per GPU."""
-    for lb in range(10, 19):
+    """Per-(op, size) lines over 1K..256K bits (every op) and 512K / 1M bits
+    (add, mul_ntt: thread-block clusters), paper batch 2^32 bits per GPU."""
+    for lb in range(10, 21):
         bits = 1 << lb
         m = bits // 32
         n = (1 << 32) // bits
@@ -434,7 +435,8 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
         o = torch.empty_like(a)
         w = work(bits)
         fns = [("add", bn.add), ("mul_classical", bn.mul_classical), ("mul_ntt", bn.mul_ntt)]
-        if not args.no_fused:
+        fns = [(k, f) for k, f in fns if bits <= bn.max_bits(k)]
+        if not args.no_fused and bits <= 262144:
             wsc, wsn = bn.poly_workspace("poly_classical", a), bn.poly_workspace("poly_ntt", a)
             wo = torch.empty((n, 2 * m), dtype=a.dtype, device=dev)
             fns += [("mul_wide_classical", lambda x, y, out: bn.mul_wide_classical(x, y, out=wo))]
@@ -477,7 +479,7 @@ def sweep(args, bn, inputs, torch, dev, rank, world, peaks, max_over_ranks, barr
             if rank == 0:
                 print(json.dumps(row), flush=True)
         del a, b, o
-        if not args.no_fused:
+        if not args.no_fused and bits <= 262144:
             del wo
         torch.cuda.empty_cache()
 

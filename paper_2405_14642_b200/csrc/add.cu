@@ -104,41 +104,65 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
 // DSMEM) — the hierarchical scan of PAPER.md:289-292 with one more level,
 // instead of the single-pass decoupled look-back over global memory the
 // paper cites.
+// Each thread stages the NEXT instance's 2 x 8 limbs into shared memory with
+// cp.async (double-buffered, 128 KiB per CTA) while it scans and stores the
+// current one, so HBM reads stay in flight across the cluster barrier; a
+// thread only ever reads back what it copied itself (no CTA barrier needed).
 template <int LOGM>
 __global__ void __launch_bounds__(1024, 1)
     add_cluster_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
                        const uint32_t* __restrict__ b, uint64_t n_inst) {
-  constexpr int M = 1 << LOGM, L = 8, CR = M / (1024 * L);
+  constexpr int M = 1 << LOGM, L = 8, CR = M / (1024 * L), SL = M / CR;  // limbs per CTA
+  extern __shared__ __align__(16) uint32_t sm[];  // [2 stages][a | b][SL]
   __shared__ uint32_t agg[32];
   __shared__ uint32_t cta_agg[2 * CR];
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   const uint64_t n_cl = gridDim.x / CR;
+  const uint32_t lo = threadIdx.x * L;
+  auto stage = [&](uint64_t inst, int st) {
+    const uint64_t off = inst * (uint64_t)M + (uint64_t)rank * SL + lo;
+    uint32_t* s = sm + st * 2 * SL;
+#pragma unroll
+    for (int v = 0; v < L / 4; v++) {
+      cp_async16(s + lo + 4 * v, a + off + 4 * v, true);
+      cp_async16(s + SL + lo + 4 * v, b + off + 4 * v, true);
+    }
+  };
+  uint64_t inst = blockIdx.x / CR;
+  if (inst < n_inst) stage(inst, 0);
+  cp_async_commit();
   int parity = 0;
-  for (uint64_t inst = blockIdx.x / CR; inst < n_inst; inst += n_cl, parity ^= 1) {
-    const uint64_t off = inst * (uint64_t)M + (uint64_t)rank * (M / CR) + (uint64_t)threadIdx.x * L;
+  for (int st = 0; inst < n_inst; inst += n_cl, parity ^= 1, st ^= 1) {
+    if (inst + n_cl < n_inst) stage(inst + n_cl, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     uint32_t x[L], y[L], r[L], g, p;
-    load_limbs<L>(x, a + off);
-    load_limbs<L>(y, b + off);
+    lds_limbs<L>(x, sm + st * 2 * SL + lo);
+    lds_limbs<L>(y, sm + st * 2 * SL + SL + lo);
     chunk_sum<L>(x, y, r, g, p);
-    if (rank == CR - 1 && threadIdx.x == 1023) g = p = 0;  // the instance's top carry-out is dropped
     const uint32_t cin = cluster_carry_scan<CR>(g, p, agg, cta_agg, parity, cl);
     chunk_apply<L>(x, r, cin);
-    store_limbs<L>(out + off, r);
+    store_limbs<L>(out + inst * (uint64_t)M + (uint64_t)rank * SL + lo, r);
   }
+  cp_async_wait<0>();
 }
 
 template <int LOGM>
 static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                         cudaStream_t st, int n_sm) {
   constexpr int CR = (1 << LOGM) / 8192;
-  const uint64_t max_cl = (uint64_t)(n_sm / CR) * 2;
+  const uint64_t max_cl = (uint64_t)(n_sm / CR);  // one 1024-thread CTA per SM
   uint64_t n_cl = n_inst < max_cl ? n_inst : max_cl;
   n_cl = cap_grid((unsigned)n_cl);
   cudaLaunchConfig_t cfg = {};
+  constexpr size_t smem = 2 * 2 * ((1 << LOGM) / CR) * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(add_cluster_kernel<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
   cfg.gridDim = dim3((unsigned)(n_cl * CR));
   cfg.blockDim = dim3(1024);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -147,7 +171,7 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, add_cluster_kernel<LOGM>, out, a, b, n_inst);
+  e = cudaLaunchKernelEx(&cfg, add_cluster_kernel<LOGM>, out, a, b, n_inst);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

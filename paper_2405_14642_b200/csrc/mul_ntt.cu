@@ -612,28 +612,38 @@ BN_DEV void xchg_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, Cluster& cl) {
     for (int e = 0; e < 16; e++) x[v][e] = X0[v * C::PL + e * C::T + threadIdx.x];
 }
 
+// Passes 1..3 keep the CTA-rank bits of gt on the top index bits, so their
+// exchanges are CTA-local and are exactly the one-CTA 2^14-point exchanges
+// (same LO values, local thread id, swizzled plane, __syncthreads); only
+// pass 0 <-> 1 goes through DSMEM.
 template <int LOGN, int NV, class Cluster>
 BN_DEV void fwd_all_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, const uint2* tw, uint32_t p, uint32_t p2,
                        Cluster& cl) {
+  using C = NttClCfg<LOGN>;
+  constexpr int L1 = PassCfg<LOGN, 1>::LO, L2 = PassCfg<LOGN, 2>::LO, L3 = PassCfg<LOGN, 3>::LO;
+  const int tid = threadIdx.x;
   fwd_pass<LOGN, 0, true, NV>(x, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 0>::LO, PassCfg<LOGN, 1>::LO, NV>(x, X0, gt, cl);
+  xchg_cl<LOGN, PassCfg<LOGN, 0>::LO, L1, NV>(x, X0, gt, cl);
   fwd_pass<LOGN, 1, true, NV>(x, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 2>::LO, NV>(x, X0, gt, cl);
+  xchg<14, L1, L2, C::T, NV, C::PL>(x, X0, 0, tid);
   fwd_pass<LOGN, 2, true, NV>(x, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 3>::LO, NV>(x, X0, gt, cl);
+  xchg<14, L2, L3, C::T, NV, C::PL>(x, X0, 0, tid);
   fwd_pass<LOGN, 3, true, NV>(x, gt, tw, p, p2);
 }
 
 template <int LOGN, class Cluster>
 BN_DEV void inv_all_cl(uint32_t (&x1)[16], uint32_t* X0, int gt, const uint2* tw, uint32_t p, uint32_t p2,
                        Cluster& cl) {
+  using C = NttClCfg<LOGN>;
+  constexpr int L1 = PassCfg<LOGN, 1>::LO, L2 = PassCfg<LOGN, 2>::LO, L3 = PassCfg<LOGN, 3>::LO;
+  const int tid = threadIdx.x;
   uint32_t(&x)[1][16] = reinterpret_cast<uint32_t(&)[1][16]>(x1);
   inv_pass<LOGN, 3>(x1, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 3>::LO, PassCfg<LOGN, 2>::LO, 1>(x, X0, gt, cl);
+  xchg<14, L3, L2, C::T, 1, C::PL>(x, X0, 0, tid);
   inv_pass<LOGN, 2>(x1, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 2>::LO, PassCfg<LOGN, 1>::LO, 1>(x, X0, gt, cl);
+  xchg<14, L2, L1, C::T, 1, C::PL>(x, X0, 0, tid);
   inv_pass<LOGN, 1>(x1, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 1>::LO, PassCfg<LOGN, 0>::LO, 1>(x, X0, gt, cl);
+  xchg_cl<LOGN, L1, PassCfg<LOGN, 0>::LO, 1>(x, X0, gt, cl);
   inv_pass<LOGN, 0>(x1, gt, tw, p, p2);
 }
 
