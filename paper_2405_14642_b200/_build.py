@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+# extra nvcc flags for A/B builds of kernel variants (e.g. -DBN_Q8_MAX_LOGM=7)
+FLAGS += os.environ.get("BN_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -124,34 +124,66 @@ constexpr uint32_t seg_top_mask() {
 }
 
 // Thread-level map + fold (PAPER.md:150-157 step (1), carry_op over the
-// thread's L limbs).  s = x + y limb-wise; returns chunk (g, p).
+// thread's L limbs), done with the hardware carry chain: s = x + y as one
+// 32L-bit sum (intra-chunk carries included), g = its carry-out (the fold's
+// generate with carry-in 0), p = "s is all ones" (the fold's propagate: a
+// carry-in would ripple through every limb).  Groups of 4 limbs per asm
+// block; the carry between groups travels in a register.
+BN_DEV uint32_t add4_cc(uint32_t (&s)[4], const uint32_t* x, const uint32_t* y, uint32_t cin) {
+  uint32_t c;
+  asm("add.cc.u32 %0, %5, 0xFFFFFFFF;\n\t"  // CC.carry = (cin != 0), cin in {0, 1}
+      "addc.cc.u32 %0, %6, %10;\n\t"
+      "addc.cc.u32 %1, %7, %11;\n\t"
+      "addc.cc.u32 %2, %8, %12;\n\t"
+      "addc.cc.u32 %3, %9, %13;\n\t"
+      "addc.u32 %4, 0, 0;"
+      : "=&r"(s[0]), "=&r"(s[1]), "=&r"(s[2]), "=&r"(s[3]), "=r"(c)
+      : "r"(cin), "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]));
+  return c;
+}
+BN_DEV uint32_t inc4_cc(uint32_t (&s)[4], uint32_t cin) {
+  uint32_t c;
+  asm("add.cc.u32 %0, %0, %5;\n\t"
+      "addc.cc.u32 %1, %1, 0;\n\t"
+      "addc.cc.u32 %2, %2, 0;\n\t"
+      "addc.cc.u32 %3, %3, 0;\n\t"
+      "addc.u32 %4, 0, 0;"
+      : "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "=r"(c)
+      : "r"(cin));
+  return c;
+}
+
 template <int L>
 BN_DEV void chunk_sum(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&s)[L], uint32_t& g,
                       uint32_t& p) {
-  g = 0;
-  p = 1;
+  static_assert(L % 4 == 0, "L must be a multiple of 4");
+  uint32_t c = 0, all = 0xFFFFFFFFu;
 #pragma unroll
-  for (int i = 0; i < L; i++) {
-    s[i] = x[i] + y[i];
-    uint32_t ov = s[i] < x[i];
-    uint32_t mx = s[i] == 0xFFFFFFFFu;
-    g = ov | (mx & g);
-    p &= mx;
+  for (int v = 0; v < L / 4; v++) {
+    uint32_t t[4];
+    c = add4_cc(t, x + 4 * v, y + 4 * v, c);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      s[4 * v + i] = t[i];
+      all &= t[i];
+    }
   }
+  g = c;
+  p = all == 0xFFFFFFFFu;
 }
 
-// Step (3): r_i = p_i + carry_i, where carry_i is the
-// exclusive scan value at limb i: the chunk's carry-in rippled through the
-// thread's own limbs together with their generates (ov) and propagates (mx).
+// Step (3): r_i = p_i + carry_i — with s already the full
+// chunk sum, the exclusive scan value at limb i is the chunk's carry-in
+// rippled through s: one carry-chain increment (x is not needed).
 template <int L>
 BN_DEV void chunk_apply(const uint32_t (&x)[L], uint32_t (&s)[L], uint32_t cin) {
+  (void)x;
 #pragma unroll
-  for (int i = 0; i < L; i++) {
-    const uint32_t ov = s[i] < x[i];
-    const uint32_t mx = s[i] == 0xFFFFFFFFu;
-    const uint32_t r = s[i] + cin;
-    cin = ov | (mx & cin);
-    s[i] = r;
+  for (int v = 0; v < L / 4; v++) {
+    uint32_t t[4] = {s[4 * v], s[4 * v + 1], s[4 * v + 2], s[4 * v + 3]};
+    cin = inc4_cc(t, cin);
+#pragma unroll
+    for (int i = 0; i < 4; i++) s[4 * v + i] = t[i];
   }
 }
 
