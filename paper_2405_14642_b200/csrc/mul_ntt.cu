@@ -32,6 +32,7 @@
 
 namespace cg = cooperative_groups;
 
+
 namespace bn {
 
 __constant__ PrimeConst c_pc[kNumPrimes];
@@ -88,7 +89,9 @@ struct NttCfg {
   // two exchange planes (A and B are transformed together), raw residues, agg
   static constexpr int SMEM_WORDS = 2 * XW + IPB * (3 * M + (TPI < 32 ? 16 : 0)) + T / 32;
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
-  static constexpr int MINB = T <= 256 ? (LOGN <= 8 ? 3 : 2) : 1;  // A/B: best of {3,4} x {2,3}
+  // (A/B on B200: best of {3,4} x {2,3} for T = 256; 2 for T = 512; T = 1024
+  // must keep 64 registers)
+  static constexpr int MINB = T <= 256 ? (LOGN <= 8 ? 3 : 2) : (T == 512 ? 2 : 1);
 };
 
 // pass P covers forward stages [S0, S1); its 16 register elements are the
