@@ -244,7 +244,7 @@ BN_DEV void st_cluster(uint32_t caddr, uint32_t v) {
 // ------------------------------------------------------- cluster carry scan
 // One instance spread over the CR CTAs of a thread-block cluster (sizes
 // beyond one CTA): CTA rank r holds the r-th contiguous
-// slice of the limbs, every CTA has 1024 threads.  Three levels of the same
+// slice of the limbs, every CTA has the same number (<= 1024) of threads.  Three levels of the same
 // carry operator (hierarchical as in PAPER.md:289-292):
 // lanes (ballot-add), warps (ballot-add over the 32 warp aggregates), CTAs
 // (each CTA's aggregate is written into every CTA's shared memory through
@@ -262,7 +262,9 @@ BN_DEV uint32_t cluster_carry_scan(uint32_t g, uint32_t p, uint32_t* agg, uint32
   const uint32_t X = G | P;
   if (lane == 0) agg[warp] = (uint32_t)(((uint64_t)X + G) >> 32) | ((P == 0xFFFFFFFFu) << 1);
   __syncthreads();
-  const uint32_t a = agg[lane];  // blockDim.x == 1024: 32 warp aggregates
+  // warp aggregates; lanes past the CTA's warp count hold the operator's
+  // identity (g = 0, p = 1), which leaves the CTA aggregate unchanged
+  const uint32_t a = lane < (blockDim.x >> 5) ? agg[lane] : 2u;
   const uint32_t G2 = __ballot_sync(0xFFFFFFFFu, a & 1u);
   const uint32_t P2 = __ballot_sync(0xFFFFFFFFu, (a >> 1) & 1u);
   const uint32_t X2 = G2 | P2;

@@ -32,6 +32,18 @@
 
 namespace cg = cooperative_groups;
 
+// Cluster NTT geometry.  A/B on B200 (scripts/ab.sh): 1024 threads per CTA
+// (64 registers, some spills) beat 512 threads per CTA at every cluster size
+// (2^18 as a 2 x 512 cluster: 8.76 ms vs 7.37 ms one CTA; 2^19: 10.9 vs 9.6;
+// 2^20: 13.3 vs 12.2), so the defaults are 1024 and one CTA up to 2^18.
+// -DBN_NTT14_CLUSTER -DBN_NTT_CL_T=512 [-DBN_NTT_CL_MINB=1] rebuild the variants.
+#ifndef BN_NTT_CL_MINB
+#define BN_NTT_CL_MINB 2
+#endif
+#ifndef BN_NTT_CL_T
+#define BN_NTT_CL_T 1024
+#endif
+
 
 namespace bn {
 
@@ -581,22 +593,26 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
 // ownership (CTA r owns coefficients [r M/CR, (r+1) M/CR)), so the CRT,
 // aggregation and L / H publish are local except one 8-word H spill per CTA,
 // and the resolve is the cluster-wide carry scan.
-template <int LOGN>
+template <int LOGN, int T_>
 struct NttClCfg {
-  static constexpr int N = 1 << LOGN, M = N / 2, T = 1024;
+  static constexpr int N = 1 << LOGN, M = N / 2, T = T_;
+  static constexpr int LT = T == 1024 ? 10 : (T == 512 ? 9 : 8);  // log2 T
   static constexpr int CR = N / (T * 16);
+  static constexpr int LB = LT + 4;   // local index bits of a CTA's slice
   static constexpr int PL = T * 16;   // words of one exchange plane per CTA
   static constexpr int MS = M / CR;   // coefficients / limbs owned by a CTA
   static constexpr int SMEM_WORDS = 2 * PL + 3 * MS + 32 + 2 * CR;
-  static_assert(CR >= 2 && MS == 8 * T, "cluster layout");
+  static constexpr int MINB = T <= 512 ? BN_NTT_CL_MINB : 1;
+  static_assert(CR >= 2 && CR <= 8 && MS == 8 * T && (1 << LT) == T, "cluster layout");
+  static_assert(PassCfg<LOGN, 1>::LO <= LT, "rank bits must sit on top of the index from pass 1 on");
 };
 
 template <int LO>
 BN_DEV int unlay_t(int u) { return (u & ((1 << LO) - 1)) | ((u >> (LO + 4)) << LO); }
 
-template <int LOGN, int LO_FROM, int LO_TO, int NV, class Cluster>
+template <int LOGN, int T, int LO_FROM, int LO_TO, int NV, class Cluster>
 BN_DEV void xchg_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, Cluster& cl) {
-  using C = NttClCfg<LOGN>;
+  using C = NttClCfg<LOGN, T>;
   cl.sync();  // every reader of every CTA's planes is done
   const uint32_t x0 = smem_addr(X0);
 #pragma unroll
@@ -619,42 +635,48 @@ BN_DEV void xchg_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, Cluster& cl) {
 // exchanges are CTA-local and are exactly the one-CTA 2^14-point exchanges
 // (same LO values, local thread id, swizzled plane, __syncthreads); only
 // pass 0 <-> 1 goes through DSMEM.
-template <int LOGN, int NV, class Cluster>
+template <int LOGN, int T, int NV, class Cluster>
 BN_DEV void fwd_all_cl(uint32_t (&x)[NV][16], uint32_t* X0, int gt, const uint2* tw, uint32_t p, uint32_t p2,
                        Cluster& cl) {
-  using C = NttClCfg<LOGN>;
-  constexpr int L1 = PassCfg<LOGN, 1>::LO, L2 = PassCfg<LOGN, 2>::LO, L3 = PassCfg<LOGN, 3>::LO;
+  using C = NttClCfg<LOGN, T>;
+  constexpr int L0 = PassCfg<LOGN, 0>::LO, L1 = PassCfg<LOGN, 1>::LO, L2 = PassCfg<LOGN, 2>::LO,
+                L3 = PassCfg<LOGN, 3>::LO;
   const int tid = threadIdx.x;
   fwd_pass<LOGN, 0, true, NV>(x, gt, tw, p, p2);
-  xchg_cl<LOGN, PassCfg<LOGN, 0>::LO, L1, NV>(x, X0, gt, cl);
+  xchg_cl<LOGN, T, L0, L1, NV>(x, X0, gt, cl);
   fwd_pass<LOGN, 1, true, NV>(x, gt, tw, p, p2);
-  xchg<14, L1, L2, C::T, NV, C::PL>(x, X0, 0, tid);
+  xchg<C::LB, L1, L2, T, NV, C::PL>(x, X0, 0, tid);
   fwd_pass<LOGN, 2, true, NV>(x, gt, tw, p, p2);
-  xchg<14, L2, L3, C::T, NV, C::PL>(x, X0, 0, tid);
-  fwd_pass<LOGN, 3, true, NV>(x, gt, tw, p, p2);
+  if constexpr (LOGN > 12) {
+    xchg<C::LB, L2, L3, T, NV, C::PL>(x, X0, 0, tid);
+    fwd_pass<LOGN, 3, true, NV>(x, gt, tw, p, p2);
+  }
 }
 
-template <int LOGN, class Cluster>
+template <int LOGN, int T, class Cluster>
 BN_DEV void inv_all_cl(uint32_t (&x1)[16], uint32_t* X0, int gt, const uint2* tw, uint32_t p, uint32_t p2,
                        Cluster& cl) {
-  using C = NttClCfg<LOGN>;
-  constexpr int L1 = PassCfg<LOGN, 1>::LO, L2 = PassCfg<LOGN, 2>::LO, L3 = PassCfg<LOGN, 3>::LO;
+  using C = NttClCfg<LOGN, T>;
+  constexpr int L0 = PassCfg<LOGN, 0>::LO, L1 = PassCfg<LOGN, 1>::LO, L2 = PassCfg<LOGN, 2>::LO,
+                L3 = PassCfg<LOGN, 3>::LO;
   const int tid = threadIdx.x;
   uint32_t(&x)[1][16] = reinterpret_cast<uint32_t(&)[1][16]>(x1);
-  inv_pass<LOGN, 3>(x1, gt, tw, p, p2);
-  xchg<14, L3, L2, C::T, 1, C::PL>(x, X0, 0, tid);
+  if constexpr (LOGN > 12) {
+    inv_pass<LOGN, 3>(x1, gt, tw, p, p2);
+    xchg<C::LB, L3, L2, T, 1, C::PL>(x, X0, 0, tid);
+  }
   inv_pass<LOGN, 2>(x1, gt, tw, p, p2);
-  xchg<14, L2, L1, C::T, 1, C::PL>(x, X0, 0, tid);
+  xchg<C::LB, L2, L1, T, 1, C::PL>(x, X0, 0, tid);
   inv_pass<LOGN, 1>(x1, gt, tw, p, p2);
-  xchg_cl<LOGN, L1, PassCfg<LOGN, 0>::LO, 1>(x, X0, gt, cl);
+  xchg_cl<LOGN, T, L1, L0, 1>(x, X0, gt, cl);
   inv_pass<LOGN, 0>(x1, gt, tw, p, p2);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(1024, 1)
+template <int LOGN, int T>
+__global__ void __launch_bounds__(T, NttClCfg<LOGN, T>::MINB)
     mul_ntt_cluster_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                            const uint2* __restrict__ tw) {
-  using C = NttClCfg<LOGN>;
+  using C = NttClCfg<LOGN, T>;
   constexpr int N = C::N, M = C::M, MS = C::MS;
   extern __shared__ __align__(16) uint32_t sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -683,11 +705,11 @@ __global__ void __launch_bounds__(1024, 1)
       }
 #pragma unroll
       for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
-      fwd_all_cl<LOGN, 2>(xab, X0, gt, twf, p, p2, cl);
+      fwd_all_cl<LOGN, T, 2>(xab, X0, gt, twf, p, p2, cl);
       uint32_t x[16];
 #pragma unroll
       for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[1][e], p, pinv);
-      inv_all_cl<LOGN>(x, X0, gt, twi, p, p2, cl);
+      inv_all_cl<LOGN, T>(x, X0, gt, twi, p, p2, cl);
       // coefficient k = gt + e N/16 (e < 8) -> its owner's residue array
 #pragma unroll
       for (int e = 0; e < 8; e++) {
@@ -761,12 +783,12 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-template <int LOGN>
+template <int LOGN, int T>
 static cudaError_t launch_ntt_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                         const NttTables& tb, cudaStream_t st, int n_sm) {
-  using C = NttClCfg<LOGN>;
+  using C = NttClCfg<LOGN, T>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(mul_ntt_cluster_kernel<LOGN>,
+  cudaError_t e = cudaFuncSetAttribute(mul_ntt_cluster_kernel<LOGN, T>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -782,13 +804,13 @@ static cudaError_t launch_ntt_cluster_t(uint32_t* out, const uint32_t* a, const 
   cfg.numAttrs = 1;
   cfg.gridDim = dim3(C::CR);
   int max_cl = 0;
-  e = cudaOccupancyMaxActiveClusters(&max_cl, mul_ntt_cluster_kernel<LOGN>, &cfg);
+  e = cudaOccupancyMaxActiveClusters(&max_cl, mul_ntt_cluster_kernel<LOGN, T>, &cfg);
   if (e != cudaSuccess) return e;
   if (max_cl < 1) return cudaErrorInvalidConfiguration;
   uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
   n_cl = cap_grid((unsigned)n_cl);
   cfg.gridDim = dim3((unsigned)(n_cl * C::CR));
-  e = cudaLaunchKernelEx(&cfg, mul_ntt_cluster_kernel<LOGN>, out, a, b, n_inst, tb.tw);
+  e = cudaLaunchKernelEx(&cfg, mul_ntt_cluster_kernel<LOGN, T>, out, a, b, n_inst, tb.tw);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -1042,8 +1064,11 @@ static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const N
 cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                            uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm) {
   switch (logm + 1) {
-    case 15: return launch_ntt_cluster_t<15>(out, a, b, n_inst, tb, st, n_sm);
-    case 16: return launch_ntt_cluster_t<16>(out, a, b, n_inst, tb, st, n_sm);
+#ifdef BN_NTT14_CLUSTER
+    case 14: return launch_ntt_cluster_t<14, 512>(out, a, b, n_inst, tb, st, n_sm);
+#endif
+    case 15: return launch_ntt_cluster_t<15, BN_NTT_CL_T>(out, a, b, n_inst, tb, st, n_sm);
+    case 16: return launch_ntt_cluster_t<16, BN_NTT_CL_T>(out, a, b, n_inst, tb, st, n_sm);
     case 6: return launch_ntt_t<6>(out, a, b, n_inst, tb, st, n_sm);
     case 7: return launch_ntt_t<7>(out, a, b, n_inst, tb, st, n_sm);
     case 8: return launch_ntt_t<8>(out, a, b, n_inst, tb, st, n_sm);
@@ -1052,7 +1077,9 @@ cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uin
     case 11: return launch_ntt_t<11>(out, a, b, n_inst, tb, st, n_sm);
     case 12: return launch_ntt_t<12>(out, a, b, n_inst, tb, st, n_sm);
     case 13: return launch_ntt_t<13>(out, a, b, n_inst, tb, st, n_sm);
+#ifndef BN_NTT14_CLUSTER
     case 14: return launch_ntt_t<14>(out, a, b, n_inst, tb, st, n_sm);
+#endif
     default: return cudaErrorInvalidValue;
   }
 }
