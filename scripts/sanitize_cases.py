@@ -1,0 +1,46 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck /
+racecheck / synccheck / initcheck): each op at a small and a large size,
+ragged batches, a grid cap so the persistent paths run, and the cluster
+sizes.  Results are checked against the oracle (any mismatch exits 1)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_2405_14642_b200 import bn, inputs  # noqa: E402
+
+dev = torch.device("cuda:0")
+bn.prepare(0)
+bad = 0
+cases = [(1024, 37), (4096, 19), (65536, 3), (262144, 1)]
+if "--big" in sys.argv:
+    cases += [(1 << 19, 2), (1 << 20, 1)]
+for cap in (0, 2):
+    bn.debug_set_grid_cap(cap)
+    for bits, n in cases:
+        m = bits // 32
+        a, b = inputs.make_operands(n, m, seed=bits + cap, cls="MIX")
+        an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+        da, db = a.to(dev), b.to(dev)
+        want = {"add": O.add(an, bnp), "mul": O.mul(an, bnp, nthreads=8)}
+        ops = [("add", bn.add), ("mul", bn.mul_ntt)]
+        if bits <= 262144:
+            want["add6"] = O.add6(an, bnp)
+            ops += [("mul", bn.mul_classical), ("add6", bn.add6)]
+            if bits <= 65536:
+                want["poly"] = O.poly(an, bnp, nthreads=8)
+                want["wide"] = O.mul_full_rows(an, bnp)
+                ops += [("poly", bn.poly_classical), ("poly", bn.poly_ntt), ("wide", bn.mul_wide_classical),
+                        ("wide", bn.mul_wide_ntt)]
+        for key, f in ops:
+            got = inputs.to_numpy_u32(f(da, db))
+            torch.cuda.synchronize()
+            if not np.array_equal(got, want[key]):
+                print("MISMATCH", f.__name__, bits, cap)
+                bad += 1
+bn.debug_set_grid_cap(0)
+print("sanitize cases done, mismatches:", bad)
+sys.exit(1 if bad else 0)
