@@ -126,6 +126,95 @@ BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_
   lhcs[Q + 1] = c_res;
 }
 
+// Squaring variant of conv_chunk (Poly's a*a and b*b): C_k = 2 sum_{i<j}
+// a_i a_j + [k even] a_{k/2}^2, so only the blocks with i < j are formed —
+// about half of them.  For column chunk j0 the full blocks c < j0/2 have
+// i < j everywhere, blocks c > j0/2 only i > j (their transposes), and the
+// single boundary block c = floor(j0/2) is masked per (row s, column q) at
+// compile time by the parity of j0 (even: 2s < q doubled, 2s = q diagonal;
+// odd: 2s - q < Q doubled, 2s - q = Q diagonal).  Off-diagonal sums are
+// doubled once at the end; diagonal squares (one per even column) go to
+// their own 64-bit accumulators.  Bsh is the same operand staged in the B
+// layout (zero prefix).
+template <int Q, int PAR>
+BN_DEV void mac_block_sqr_edge(uint32_t (&lo)[Q], uint32_t (&hi)[Q], uint32_t (&top)[Q], uint32_t (&dlo)[Q],
+                               uint32_t (&dhi)[Q], const uint32_t (&av)[Q], const uint32_t (&cur)[Q],
+                               const uint32_t (&prev)[Q]) {
+#pragma unroll
+  for (int s = 0; s < Q; s++) {
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int d = q - s;
+      const int key = 2 * s - q - (PAR ? Q : 0);  // < 0: doubled, == 0: diagonal
+      if (key < 0) {
+        mac3(lo[q], hi[q], top[q], av[s], d >= 0 ? cur[d] : prev[Q + d]);
+      } else if (key == 0) {
+        uint32_t t = 0;
+        mac3(dlo[q], dhi[q], t, av[s], d >= 0 ? cur[d] : prev[Q + d]);
+      }
+    }
+  }
+}
+
+template <int Q>
+BN_DEV void conv_chunk_sqr(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_t (&lhcs)[Q + 2]) {
+  uint32_t lo[Q], hi[Q], top[Q], dlo[Q], dhi[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) lo[q] = hi[q] = top[q] = dlo[q] = dhi[q] = 0;
+  uint32_t b0[Q], b1[Q], av[Q];
+  lds_limbs<Q>(b0, Bsh + Q * j0);
+  const uint32_t* ap = Ash;
+  const uint32_t* bp = Bsh + Q * (j0 - 1);
+  const int cm = j0 >> 1;  // boundary block
+  int c = cm;              // full blocks before it
+#pragma unroll 1
+  for (; c >= 2; c -= 2) {
+    lds_limbs<Q>(av, ap);
+    lds_limbs<Q>(b1, bp);
+    mac_block<Q>(lo, hi, top, av, b0, b1);
+    lds_limbs<Q>(av, ap + Q);
+    lds_limbs<Q>(b0, bp - Q);
+    mac_block<Q>(lo, hi, top, av, b1, b0);
+    ap += 2 * Q;
+    bp -= 2 * Q;
+  }
+  if (c) {  // one more full block: the window roles swap for the edge
+    lds_limbs<Q>(av, ap);
+    lds_limbs<Q>(b1, bp);
+    mac_block<Q>(lo, hi, top, av, b0, b1);
+    lds_limbs<Q>(av, ap + Q);
+    lds_limbs<Q>(b0, bp - Q);
+    if (j0 & 1) mac_block_sqr_edge<Q, 1>(lo, hi, top, dlo, dhi, av, b1, b0);
+    else mac_block_sqr_edge<Q, 0>(lo, hi, top, dlo, dhi, av, b1, b0);
+  } else {
+    lds_limbs<Q>(av, ap);
+    lds_limbs<Q>(b1, bp);
+    if (j0 & 1) mac_block_sqr_edge<Q, 1>(lo, hi, top, dlo, dhi, av, b0, b1);
+    else mac_block_sqr_edge<Q, 0>(lo, hi, top, dlo, dhi, av, b0, b1);
+  }
+  // column sums: 2 * (lo, hi, top) + (dlo, dhi)
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const uint32_t t2 = (top[q] << 1) | (hi[q] >> 31);
+    const uint32_t t1 = (hi[q] << 1) | (lo[q] >> 31);
+    const uint32_t t0 = lo[q] << 1;
+    asm("add.cc.u32 %0, %3, %4;\n\taddc.cc.u32 %1, %5, %6;\n\taddc.u32 %2, %7, 0;"
+        : "=r"(lo[q]), "=r"(hi[q]), "=r"(top[q])
+        : "r"(t0), "r"(dlo[q]), "r"(t1), "r"(dhi[q]), "r"(t2));
+  }
+  lhcs[0] = lo[0];
+  uint32_t h_res = hi[0], c_res = top[0];
+#pragma unroll
+  for (int q = 1; q < Q; q++) {
+    const uint32_t l = lo[q], h = hi[q];
+    lhcs[q] = l + h_res;
+    h_res = h + (c_res + (lhcs[q] < l));
+    c_res = top[q] + (h_res < h);
+  }
+  lhcs[Q] = h_res;
+  lhcs[Q + 1] = c_res;
+}
+
 // Thread roles inside a CTA (see MulCCfg): the convolution mapping
 // interleaves instances across warp lanes; the resolve mapping is
 // instance-major with G consecutive threads per instance.
@@ -171,7 +260,7 @@ BN_DEV void stage_xy(uint32_t* As, const uint32_t* x, const uint32_t* y, uint64_
 
 // Convolution (Fig. 7) of the staged group and the L/H publish (reading R8),
 // L over the A area, H over the B area.  Ends with a CTA barrier.
-template <class C>
+template <class C, bool SQ = false>
 BN_DEV void conv_publish(uint32_t* As, const MulCRoles<C>& ro) {
   constexpr int M = C::M, Q = C::Q;
   uint32_t* Bs = As + C::IPB * C::SA;
@@ -180,8 +269,13 @@ BN_DEV void conv_publish(uint32_t* As, const MulCRoles<C>& ro) {
   {
     const uint32_t* Ai = As + ro.conv_slot * C::SA;
     const uint32_t* Bi = Bs + ro.conv_slot * C::SB + Q;
-    conv_chunk<Q>(Ai, Bi, ro.g, lh0);
-    conv_chunk<Q>(Ai, Bi, M / Q - 1 - ro.g, lh1);
+    if constexpr (SQ) {
+      conv_chunk_sqr<Q>(Ai, Bi, ro.g, lh0);
+      conv_chunk_sqr<Q>(Ai, Bi, M / Q - 1 - ro.g, lh1);
+    } else {
+      conv_chunk<Q>(Ai, Bi, ro.g, lh0);
+      conv_chunk<Q>(Ai, Bi, M / Q - 1 - ro.g, lh1);
+    }
   }
   __syncthreads();
   // ---- publish (reading R8): L[k1+q] = low_q; H[k1+Q] = high; H[k1+Q+1] = carry;
@@ -350,7 +444,7 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
 // CTA) and come back as the operands of the last phase.
 //   phase 1: t1 = a*a + b    phase 2: t2 = b*b + b
 //   phase 3: t3 = a*b        phase 4: out = t1*t2 + t3
-template <class C, bool AWS, bool OWS>
+template <class C, bool AWS, bool OWS, bool SQ = false>
 BN_DEV void classical_phase(uint32_t* As, uint32_t* agg, const MulCRoles<C>& ro, const uint32_t* x,
                             const uint32_t* y, const uint32_t* addend, uint32_t* dst, uint64_t n_valid) {
   constexpr int Q = C::Q, M = C::M;
@@ -358,7 +452,7 @@ BN_DEV void classical_phase(uint32_t* As, uint32_t* agg, const MulCRoles<C>& ro,
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  conv_publish<C>(As, ro);
+  conv_publish<C, SQ>(As, ro);
   const bool valid = (uint64_t)ro.add_slot < n_valid;
   const uint64_t off = (uint64_t)ro.add_slot * M + 2 * Q * ro.chunk;
   uint32_t res[2 * Q];
@@ -399,8 +493,8 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
     const uint64_t nv = n_inst - i0 < (uint64_t)C::IPB ? n_inst - i0 : (uint64_t)C::IPB;
     const uint32_t* ag = a + i0 * M;
     const uint32_t* bg = b + i0 * M;
-    classical_phase<C, false, true>(sm, agg, ro, ag, ag, bg, t1, nv);
-    classical_phase<C, false, true>(sm, agg, ro, bg, bg, bg, t2, nv);
+    classical_phase<C, false, true, true>(sm, agg, ro, ag, ag, bg, t1, nv);  // squares: half
+    classical_phase<C, false, true, true>(sm, agg, ro, bg, bg, bg, t2, nv);  // the blocks
     classical_phase<C, false, true>(sm, agg, ro, ag, bg, nullptr, t3, nv);
     classical_phase<C, true, false>(sm, agg, ro, t1, t2, t3, out + i0 * M, nv);
   }

@@ -251,3 +251,48 @@ def test_ntt_model(m):
     for A, B in cases:
         want = from_int(to_int(A) * to_int(B) % (1 << (32 * m)), m)
         assert model_ntt_mul(A, B) == want
+
+
+# ---------------------------------------------------------------------------
+# Squaring block selection of conv_chunk_sqr (mul_classical.cu, Poly's a*a
+# and b*b): for every column chunk j0, the full blocks c < j0//2 plus the
+# parity-masked boundary block c = j0//2 must form each pair i < j of the
+# column exactly once (doubled) and the diagonal i == j once (single) —
+# against the definition sum_{i+j=k} a_i a_j, exhaustively for small sizes.
+
+def _sqr_chunk_terms(j0, Q):
+    """(k, i, j, weight) terms the kernel forms for column chunk j0."""
+    terms = []
+    cm = j0 // 2
+    for c in range(cm + 1):
+        for s in range(Q):
+            for q in range(Q):
+                i = Q * c + s
+                k = Q * j0 + q
+                j = k - i
+                if j < 0:
+                    continue  # B's zero prefix
+                if c < cm:
+                    terms.append((k, i, j, 2))
+                else:
+                    key = 2 * s - q - (Q if j0 & 1 else 0)
+                    if key < 0:
+                        terms.append((k, i, j, 2))
+                    elif key == 0:
+                        terms.append((k, i, j, 1))
+    return terms
+
+
+@pytest.mark.parametrize("M,Q", [(16, 4), (32, 4), (64, 4), (32, 8), (64, 8)])
+def test_square_block_selection(M, Q):
+    rng = random.Random(M * Q)
+    a = [rng.getrandbits(32) for _ in range(M)]
+    for j0 in range(M // Q):
+        got = {}
+        for k, i, j, w in _sqr_chunk_terms(j0, Q):
+            assert i < j or (i == j and w == 1), (j0, k, i, j, w)
+            got[k] = got.get(k, 0) + w * a[i] * a[j]
+        for q in range(Q):
+            k = Q * j0 + q
+            want = sum(a[i] * a[k - i] for i in range(k + 1))
+            assert got.get(k, 0) == want, (M, Q, j0, k)
