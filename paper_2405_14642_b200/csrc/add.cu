@@ -21,6 +21,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef BN_ADD_CL_STAGES
+#define BN_ADD_CL_STAGES 2  // cp.async stages of the cluster add (64 KiB each; 3 measured no faster)
+#endif
+
 namespace bn {
 
 template <int LOGM, int L>
@@ -104,16 +108,18 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
 // DSMEM) — the hierarchical scan of PAPER.md:289-292 with one more level,
 // instead of the single-pass decoupled look-back over global memory the
 // paper cites.
-// Each thread stages the NEXT instance's 2 x 8 limbs into shared memory with
-// cp.async (double-buffered, 128 KiB per CTA) while it scans and stores the
-// current one, so HBM reads stay in flight across the cluster barrier; a
-// thread only ever reads back what it copied itself (no CTA barrier needed).
+// Each thread stages the next NS - 1 instances' 2 x 8 limbs into shared
+// memory with cp.async (NS stages of 64 KiB per CTA) while it scans and
+// stores the current one, so HBM reads stay in flight across the cluster
+// barriers; a thread only ever reads back what it copied itself (no CTA
+// barrier needed).
 template <int LOGM>
 __global__ void __launch_bounds__(1024, 1)
     add_cluster_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
                        const uint32_t* __restrict__ b, uint64_t n_inst) {
   constexpr int M = 1 << LOGM, L = 8, CR = M / (1024 * L), SL = M / CR;  // limbs per CTA
-  extern __shared__ __align__(16) uint32_t sm[];  // [2 stages][a | b][SL]
+  constexpr int NS = BN_ADD_CL_STAGES;            // instances in flight + 1
+  extern __shared__ __align__(16) uint32_t sm[];  // [NS stages][a | b][SL]
   __shared__ uint32_t agg[32];
   __shared__ uint32_t cta_agg[2 * CR];
   cg::cluster_group cl = cg::this_cluster();
@@ -130,13 +136,18 @@ __global__ void __launch_bounds__(1024, 1)
     }
   };
   uint64_t inst = blockIdx.x / CR;
-  if (inst < n_inst) stage(inst, 0);
-  cp_async_commit();
-  int parity = 0;
-  for (int st = 0; inst < n_inst; inst += n_cl, parity ^= 1, st ^= 1) {
-    if (inst + n_cl < n_inst) stage(inst + n_cl, st ^ 1);
+  // prologue: the first NS - 1 instances in flight
+#pragma unroll
+  for (int k = 0; k < NS - 1; k++) {
+    if (inst + k * n_cl < n_inst) stage(inst + k * n_cl, k);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  int parity = 0;
+  for (int st = 0; inst < n_inst; inst += n_cl, parity ^= 1, st = st == NS - 1 ? 0 : st + 1) {
+    const int sf = st == 0 ? NS - 1 : st - 1;  // stage of instance inst + (NS-1) n_cl
+    if (inst + (NS - 1) * n_cl < n_inst) stage(inst + (NS - 1) * n_cl, sf);
+    cp_async_commit();
+    cp_async_wait<NS - 1>();
     uint32_t x[L], y[L], r[L], g, p;
     lds_limbs<L>(x, sm + st * 2 * SL + lo);
     lds_limbs<L>(y, sm + st * 2 * SL + SL + lo);
@@ -152,15 +163,12 @@ template <int LOGM>
 static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                         cudaStream_t st, int n_sm) {
   constexpr int CR = (1 << LOGM) / 8192;
-  const uint64_t max_cl = (uint64_t)(n_sm / CR);  // one 1024-thread CTA per SM
-  uint64_t n_cl = n_inst < max_cl ? n_inst : max_cl;
-  n_cl = cap_grid((unsigned)n_cl);
   cudaLaunchConfig_t cfg = {};
-  constexpr size_t smem = 2 * 2 * ((1 << LOGM) / CR) * sizeof(uint32_t);
+  constexpr size_t smem = BN_ADD_CL_STAGES * 2 * ((1 << LOGM) / CR) * sizeof(uint32_t);
   cudaError_t e = cudaFuncSetAttribute(add_cluster_kernel<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  cfg.gridDim = dim3((unsigned)(n_cl * CR));
+  cfg.gridDim = dim3(CR);
   cfg.blockDim = dim3(1024);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -171,6 +179,16 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // persistent clusters: exactly as many as can be co-resident (clusters must
+  // fit in one GPC, so this is below n_sm / CR); more would run as a second
+  // wave and double the time
+  int max_cl = 0;
+  e = cudaOccupancyMaxActiveClusters(&max_cl, add_cluster_kernel<LOGM>, &cfg);
+  if (e != cudaSuccess) return e;
+  if (max_cl < 1) return cudaErrorInvalidConfiguration;
+  uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
+  n_cl = cap_grid((unsigned)n_cl);
+  cfg.gridDim = dim3((unsigned)(n_cl * CR));
   e = cudaLaunchKernelEx(&cfg, add_cluster_kernel<LOGM>, out, a, b, n_inst);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
