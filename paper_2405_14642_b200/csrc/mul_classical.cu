@@ -27,6 +27,10 @@
 #include "bn_common.cuh"
 #include "bn_kernels.h"
 
+#ifndef BN_CLASSICAL_MINB
+#define BN_CLASSICAL_MINB 2  // 2 x 512-thread CTAs per SM (64 registers)
+#endif
+
 namespace bn {
 
 BN_DEV void mac3(uint32_t& lo, uint32_t& hi, uint32_t& top, uint32_t a, uint32_t b) {
@@ -55,7 +59,7 @@ struct MulCCfg {
   static constexpr int SB = M + Q + (((4 * BS - Q) % 32) + 32) % 32;
   static constexpr int STAGE_WORDS = IPB * (SA + SB);      // one group's A and B
   static constexpr int SMEM_WORDS = 2 * STAGE_WORDS + T / 32;  // double-buffered
-  static constexpr int MINB = T >= 1024 ? 1 : 2048 / T / 2;    // target residency
+  static constexpr int MINB = T >= 1024 ? 1 : BN_CLASSICAL_MINB;  // target residency
   static_assert(Q >= 2 && (Q % 4) == 0, "Q must be a multiple of 4 (>= 2 for the L/H layout)");
   static_assert(G >= 1, "size too small for Q");
 };
