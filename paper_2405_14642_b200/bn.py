@@ -123,12 +123,32 @@ def _check(a: torch.Tensor, b: torch.Tensor, out):
     return out
 
 
+class _on_device:
+    """Make `dev` the current CUDA device for a C-ABI call (the library
+    launches on the current device) — a no-op when it already is, which
+    keeps the per-call host cost low for small batches."""
+
+    __slots__ = ("dev", "prev")
+
+    def __init__(self, dev: torch.device):
+        self.dev = dev.index
+
+    def __enter__(self):
+        self.prev = torch.cuda.current_device()
+        if self.prev != self.dev:
+            torch.cuda.set_device(self.dev)
+        return torch._C._cuda_getCurrentRawStream(self.dev)
+
+    def __exit__(self, *exc):
+        if self.prev != self.dev:
+            torch.cuda.set_device(self.prev)
+
+
 def _call(name: str, a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
     out = _check(a, b, out)
-    lib = load()
+    lib = _lib if _lib is not None else load()
     n_inst, n_limbs = a.shape
-    with torch.cuda.device(a.device):
-        stream = torch.cuda.current_stream(a.device).cuda_stream
+    with _on_device(a.device) as stream:
         st = getattr(lib, name)(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs,
                                 _limb_bits(a), stream)
     if st != 0:
@@ -160,8 +180,7 @@ def _wide(name: str, a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor
             or not out.is_contiguous():
         raise ValueError("out must be [n_inst, 2*n_limbs], a's dtype and device, contiguous")
     lib = load()
-    with torch.cuda.device(a.device):
-        stream = torch.cuda.current_stream(a.device).cuda_stream
+    with _on_device(a.device) as stream:
         st = getattr(lib, name)(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs,
                                 _limb_bits(a), stream)
     if st != 0:
@@ -204,8 +223,7 @@ def _poly(name: str, op: str, a, b, out, workspace):
         raise ValueError("workspace must be a contiguous CUDA tensor on the operands' device")
     lib = load()
     n_inst, n_limbs = a.shape
-    with torch.cuda.device(a.device):
-        stream = torch.cuda.current_stream(a.device).cuda_stream
+    with _on_device(a.device) as stream:
         st = getattr(lib, name)(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs, _limb_bits(a),
                                 workspace.data_ptr(), workspace.numel() * workspace.element_size(), stream)
     if st != 0:

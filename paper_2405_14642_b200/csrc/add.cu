@@ -165,9 +165,6 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   constexpr int CR = (1 << LOGM) / 8192;
   cudaLaunchConfig_t cfg = {};
   constexpr size_t smem = BN_ADD_CL_STAGES * 2 * ((1 << LOGM) / CR) * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(add_cluster_kernel<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
   cfg.gridDim = dim3(CR);
   cfg.blockDim = dim3(1024);
   cfg.dynamicSmemBytes = smem;
@@ -182,8 +179,13 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   // persistent clusters: exactly as many as can be co-resident (clusters must
   // fit in one GPC, so this is below n_sm / CR); more would run as a second
   // wave and double the time
+  static LaunchCache cache;
   int max_cl = 0;
-  e = cudaOccupancyMaxActiveClusters(&max_cl, add_cluster_kernel<LOGM>, &cfg);
+  cudaError_t e = cached_query(cache, [&](int* o) {
+    cudaError_t e1 = cudaFuncSetAttribute(add_cluster_kernel<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e1 != cudaSuccess) return e1;
+    return cudaOccupancyMaxActiveClusters(o, add_cluster_kernel<LOGM>, &cfg);
+  }, &max_cl);
   if (e != cudaSuccess) return e;
   if (max_cl < 1) return cudaErrorInvalidConfiguration;
   uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;

@@ -1,6 +1,7 @@
 // bn_kernels.h — internal interface between the host dispatcher (bn_api.cu)
 // and the kernel translation units.  Not part of the public C ABI.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -41,6 +42,41 @@ struct NttTables {
   const uint2* tw;
   uint32_t omega[kNumPrimes];  // primitive N-th roots used (host side; debug/tests)
 };
+
+// Per-device cache of a launch-geometry query (cudaFuncSetAttribute for the
+// dynamic shared memory + an occupancy query): microseconds per call on the
+// host, and the answer never changes for a (kernel instantiation, device).
+// One static LaunchCache per call site; 0 = not yet known.
+struct LaunchCache {
+  std::atomic<int> v[64];
+};
+template <class Query>
+inline cudaError_t cached_query(LaunchCache& c, Query&& q, int* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const bool ok = dev >= 0 && dev < 64;
+  if (ok) {
+    const int v = c.v[dev].load(std::memory_order_relaxed);
+    if (v > 0) {
+      *out = v;
+      return cudaSuccess;
+    }
+  }
+  e = q(out);
+  if (e == cudaSuccess && ok && *out > 0) c.v[dev].store(*out, std::memory_order_relaxed);
+  return e;
+}
+// resident CTAs per SM of `kernel` with `threads` threads and `smem` bytes of
+// dynamic shared memory (sets the opt-in shared-memory limit on first use)
+template <class K>
+inline cudaError_t resident_ctas(LaunchCache& c, K kernel, int threads, size_t smem, int* per_sm) {
+  return cached_query(c, [&](int* o) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(o, kernel, threads, smem);
+  }, per_sm);
+}
 
 // prime constants + per-lg CRT constants -> __constant__ memory of the current device
 // Test knob (bn_debug_set_grid_cap): when > 0, every launcher caps its grid

@@ -633,13 +633,11 @@ static cudaError_t launch_mulw_t(uint32_t* out, const uint32_t* a, const uint32_
   constexpr int Q = 4;
   using C = MulWCfg<LOGM, Q>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(mul_wide_classical_kernel<LOGM, Q>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static LaunchCache cache;
+  int per_sm = 0;
+  cudaError_t e = resident_ctas(cache, mul_wide_classical_kernel<LOGM, Q>, C::T, smem, &per_sm);
   if (e != cudaSuccess) return e;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_wide_classical_kernel<LOGM, Q>, C::T, smem);
-  if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t cap = (uint64_t)n_sm * per_sm * 4;
   const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
@@ -653,13 +651,11 @@ static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_
   constexpr int Q = 4;
   using C = MulCCfg<LOGM, Q>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(mul_classical_kernel<LOGM, Q>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static LaunchCache cache;
+  int per_sm = 0;
+  cudaError_t e = resident_ctas(cache, mul_classical_kernel<LOGM, Q>, C::T, smem, &per_sm);
   if (e != cudaSuccess) return e;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_classical_kernel<LOGM, Q>, C::T, smem);
-  if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t cap = (uint64_t)n_sm * per_sm;  // persistent: one wave of resident CTAs
   const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
@@ -673,11 +669,9 @@ static cudaError_t poly_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64
   constexpr int Q = 4;
   using C = MulCCfg<LOGM, Q>;
   constexpr size_t smem = (C::STAGE_WORDS + C::T / 32) * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(poly_classical_kernel<LOGM, Q>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static LaunchCache cache;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, poly_classical_kernel<LOGM, Q>, C::T, smem);
+  cudaError_t e = resident_ctas(cache, poly_classical_kernel<LOGM, Q>, C::T, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;

@@ -788,9 +788,6 @@ static cudaError_t launch_ntt_cluster_t(uint32_t* out, const uint32_t* a, const 
                                         const NttTables& tb, cudaStream_t st, int n_sm) {
   using C = NttClCfg<LOGN, T>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(mul_ntt_cluster_kernel<LOGN, T>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(C::T);
   cfg.dynamicSmemBytes = smem;
@@ -803,8 +800,13 @@ static cudaError_t launch_ntt_cluster_t(uint32_t* out, const uint32_t* a, const 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.gridDim = dim3(C::CR);
+  static LaunchCache cache;
   int max_cl = 0;
-  e = cudaOccupancyMaxActiveClusters(&max_cl, mul_ntt_cluster_kernel<LOGN, T>, &cfg);
+  cudaError_t e = cached_query(cache, [&](int* o) {
+    cudaError_t e1 = cudaFuncSetAttribute(mul_ntt_cluster_kernel<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e1 != cudaSuccess) return e1;
+    return cudaOccupancyMaxActiveClusters(o, mul_ntt_cluster_kernel<LOGN, T>, &cfg);
+  }, &max_cl);
   if (e != cudaSuccess) return e;
   if (max_cl < 1) return cudaErrorInvalidConfiguration;
   uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
@@ -951,13 +953,11 @@ static cudaError_t launch_wide_ntt_t(uint32_t* out, const uint32_t* a, const uin
   } else {
     using C = NttCfg<LOGN>;
     constexpr size_t smem = NttWideCfg<LOGN>::SMEM_WORDS * sizeof(uint32_t);
-    cudaError_t e = cudaFuncSetAttribute(mul_wide_ntt_kernel<LOGN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static LaunchCache cache;
+    int per_sm = 0;
+    cudaError_t e = resident_ctas(cache, mul_wide_ntt_kernel<LOGN>, C::T, smem, &per_sm);
     if (e != cudaSuccess) return e;
     const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_wide_ntt_kernel<LOGN>, C::T, smem);
-    if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
     const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
@@ -1000,13 +1000,11 @@ static cudaError_t launch_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t
                                 const NttTables& tb, cudaStream_t st, int n_sm) {
   using C = NttCfg<LOGN>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(mul_ntt_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  static LaunchCache cache;
+  int per_sm = 0;
+  cudaError_t e = resident_ctas(cache, mul_ntt_kernel<LOGN>, C::T, smem, &per_sm);
   if (e != cudaSuccess) return e;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mul_ntt_kernel<LOGN>, C::T, smem);
-  if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
   const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
@@ -1018,11 +1016,9 @@ template <int LOGN>
 static cudaError_t poly_ntt_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64_t* ws_words) {
   using C = NttCfg<LOGN>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(poly_ntt_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  static LaunchCache cache;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, poly_ntt_kernel<LOGN>, C::T, smem);
+  cudaError_t e = resident_ctas(cache, poly_ntt_kernel<LOGN>, C::T, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
