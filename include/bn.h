@@ -19,9 +19,10 @@
  * paper's 2^11..2^18 sweep, PAPER.md:919 and Tables 1-2, plus 2^10), one
  * instance (or several) per CTA: 262144 bits is the largest size whose exact
  * NTT product fits one CTA's shared memory.  bn_add and bn_mul_ntt go on to
- * 2^19 and 2^20 bits with one instance per thread-block cluster of 2 / 4
- * CTAs (carries and NTT exchanges through distributed shared memory,
- * DESIGN.md §7d); bn_mul_wide_ntt stops at 2^17.  Other sizes -> BN_ESIZE.
+ * 2^19 and 2^20 bits, bn_mul_classical to 2^19, with one instance per
+ * thread-block cluster of 2 / 4 CTAs (carries, NTT exchanges and the L/H
+ * publish through distributed shared memory);
+ * bn_mul_wide_ntt stops at 2^17.  Other sizes -> BN_ESIZE.
  *
  * POINTERS: a, b, out are DEVICE pointers on the current CUDA device, 16-byte
  * aligned.  out may equal a or b exactly (in-place); a partial overlap is

@@ -24,8 +24,12 @@
 //    small sizes I instances are interleaved across the lanes of a warp so
 //    that lanes of a warp have (nearly) the same trip count: divergence
 //    overhead (C-1)Q/(M+Q) with C = 32/I column groups per warp (<= 3%).
+#include <cooperative_groups.h>
+
 #include "bn_common.cuh"
 #include "bn_kernels.h"
+
+namespace cg = cooperative_groups;
 
 #ifndef BN_CLASSICAL_MINB
 #define BN_CLASSICAL_MINB 2  // 2 x 512-thread CTAs per SM (64 registers)
@@ -726,6 +730,121 @@ cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, co
   BN_LOGM_SWITCH(launch_polyc_t, out, a, b, n_inst, ws, ws_words, st, n_sm)
 }
 
+// ------------------------------------------------------------ beyond one CTA
+// 2^19 bits (m = 16384): one instance per cluster of 2 CTAs
+// x 1024 threads.  Every CTA stages the whole of A and B (64 KiB each) —
+// every chunk pair needs both operands in full — and global thread
+// g = rank * 1024 + tid runs the Fig. 5 chunk pair (g, M/Q - 1 - g) exactly
+// as the one-CTA kernel (Q = 4, G = 2048).  After a cluster barrier (no CTA
+// may overwrite a peer's A/B while it convolves) the L/H publish goes to the
+// CTA owning those limbs (CTA r owns [r M/2, (r+1) M/2); a chunk's Q-word runs
+// never straddle owners) through DSMEM, and the resolve is the cluster carry
+// scan.  2^20 bits would need 256 KiB of operands per CTA: not supported.
+struct MulClCfg {
+  static constexpr int LOGM = 14, M = 1 << LOGM, Q = 4, T = 1024, CR = 2;
+  static constexpr int MS = M / CR;          // limbs owned (and resolved) per CTA
+  static constexpr int SA = M + 4;           // A | L (owned half)
+  static constexpr int SB = M + 2 * Q;       // Q zeros | B, H (owned half) at +Q
+  static constexpr int SMEM_WORDS = SA + SB + 32 + 2 * CR;
+  static_assert(MS == 8 * T && M / (2 * Q) == CR * T, "cluster classical layout");
+};
+
+BN_DEV void st_cluster_v4(uint32_t caddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(caddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(1024, 1)
+    mul_classical_cluster_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
+  using C = MulClCfg;
+  constexpr int M = C::M, Q = C::Q, MS = C::MS;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* As = sm;
+  uint32_t* Bs = sm + C::SA;  // B[x] at Bs[Q + x]
+  uint32_t* agg = Bs + C::SB;
+  uint32_t* cta_agg = agg + 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const int g = rank * C::T + tid;
+  if (tid < Q) Bs[tid] = 0u;  // B[-Q..-1] = 0, never overwritten
+  const uint64_t n_cl = gridDim.x / C::CR;
+  int parity = 0;
+  for (uint64_t inst = blockIdx.x / C::CR; inst < n_inst; inst += n_cl, parity ^= 1) {
+    // stage A and B (each CTA its own copy; the peer's copy hits L2)
+    const uint32_t* ai = a + inst * M;
+    const uint32_t* bi = b + inst * M;
+    for (int v = tid; v < M / 4; v += C::T) {
+      cp_async16(As + 4 * v, ai + 4 * v, true);
+      cp_async16(Bs + Q + 4 * v, bi + 4 * v, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // convolution: chunk pair (g, M/Q - 1 - g)
+    uint32_t lh0[Q + 2], lh1[Q + 2];
+    conv_chunk<Q>(As, Bs + Q, g, lh0);
+    conv_chunk<Q>(As, Bs + Q, M / Q - 1 - g, lh1);
+    cl.sync();  // every CTA is done reading its A / B: L / H may overwrite them
+    // publish into the owner's L (A area) / H (B area + Q), local index
+    const uint32_t la = smem_addr(As), ha = smem_addr(Bs + Q);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t* lh = h == 0 ? lh0 : lh1;
+      const int k1 = Q * (h == 0 ? g : M / Q - 1 - g);
+      st_cluster_v4(mapa_rank(la + 4 * (k1 % MS), k1 / MS), lh[0], lh[1], lh[2], lh[3]);
+      const int kh = k1 + Q < M ? k1 + Q : 0;  // top chunk: zeroes H[0, Q)
+      const uint32_t h0 = k1 + Q < M ? lh[Q] : 0u, h1 = k1 + Q < M ? lh[Q + 1] : 0u;
+      st_cluster_v4(mapa_rank(ha + 4 * (kh % MS), kh / MS), h0, h1, 0u, 0u);
+    }
+    cl.sync();
+    // resolve this CTA's limbs [rank MS + 8 tid, +8)
+    uint32_t x[8], y[8], r[8], gg, pp;
+    lds_limbs<8>(x, As + 8 * tid);
+    lds_limbs<8>(y, Bs + Q + 8 * tid);
+    chunk_sum<8>(x, y, r, gg, pp);
+    const uint32_t cin = cluster_carry_scan<C::CR>(gg, pp, agg, cta_agg, parity, cl);
+    chunk_apply<8>(x, r, cin);
+    store_limbs<8>(out + inst * M + (uint64_t)rank * MS + 8 * tid, r);
+    __syncthreads();  // L / H reads done before the next instance's staging
+  }
+}
+
+static cudaError_t launch_mulc_cluster(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                       cudaStream_t st, int n_sm) {
+  using C = MulClCfg;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.gridDim = dim3(C::CR);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CR;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static LaunchCache cache;
+  int max_cl = 0;
+  cudaError_t e = cached_query(cache, [&](int* o) {
+    cudaError_t e1 = cudaFuncSetAttribute(mul_classical_cluster_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e1 != cudaSuccess) return e1;
+    return cudaOccupancyMaxActiveClusters(o, mul_classical_cluster_kernel, &cfg);
+  }, &max_cl);
+  if (e != cudaSuccess) return e;
+  if (max_cl < 1) return cudaErrorInvalidConfiguration;
+  uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
+  n_cl = cap_grid((unsigned)n_cl);
+  cfg.gridDim = dim3((unsigned)(n_cl * C::CR));
+  e = cudaLaunchKernelEx(&cfg, mul_classical_cluster_kernel, out, a, b, n_inst);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                  uint64_t n_inst, cudaStream_t st, int n_sm) {
   switch (logm) {
@@ -738,6 +857,7 @@ cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, con
     case 11: return launch_mulc_t<11>(out, a, b, n_inst, st, n_sm);
     case 12: return launch_mulc_t<12>(out, a, b, n_inst, st, n_sm);
     case 13: return launch_mulc_t<13>(out, a, b, n_inst, st, n_sm);
+    case 14: return launch_mulc_cluster(out, a, b, n_inst, st, n_sm);
     default: return cudaErrorInvalidValue;
   }
 }

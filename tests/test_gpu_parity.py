@@ -452,9 +452,17 @@ def test_parity_cluster_sizes(bits, cls):
     got = inputs.to_numpy_u32(bn.add(da, db))
     bad = _first_bad(got, O.add(an, bnp))
     assert bad is None, "add %d %s: %s" % (bits, cls, bad)
+    wm = O.mul(an, bnp, nthreads=8)
     got = inputs.to_numpy_u32(bn.mul_ntt(da, db))
-    bad = _first_bad(got, O.mul(an, bnp, nthreads=8))
+    bad = _first_bad(got, wm)
     assert bad is None, "mul_ntt %d %s: %s" % (bits, cls, bad)
+    if bits <= bn.max_bits("mul_classical"):
+        got = inputs.to_numpy_u32(bn.mul_classical(da, db))
+        bad = _first_bad(got, wm)
+        assert bad is None, "mul_classical %d %s: %s" % (bits, cls, bad)
+    else:
+        with pytest.raises(bn.BnError):
+            bn.mul_classical(da, db)
 
 
 @pytest.mark.parametrize("bits", CLUSTER_SIZES)
@@ -490,7 +498,10 @@ def test_cluster_grid_cap(cap):
     try:
         ga = inputs.to_numpy_u32(bn.add(da, db))
         gm = inputs.to_numpy_u32(bn.mul_ntt(da, db))
+        gc = inputs.to_numpy_u32(bn.mul_classical(da, db))
     finally:
         bn.debug_set_grid_cap(0)
+    wm = O.mul(an, bnp, nthreads=8)
     assert _first_bad(ga, O.add(an, bnp)) is None
-    assert _first_bad(gm, O.mul(an, bnp, nthreads=8)) is None
+    assert _first_bad(gm, wm) is None
+    assert _first_bad(gc, wm) is None
