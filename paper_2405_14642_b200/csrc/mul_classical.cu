@@ -92,7 +92,10 @@ BN_DEV void mac_block(uint32_t (&lo)[Q], uint32_t (&hi)[Q], uint32_t (&top)[Q], 
 // half (mul_wide_classical_kernel), whose column Q j0 + q is the original
 // column 2M - 1 - Q j0 - q: combine then runs over q descending so lhcs is
 // in ascending original order.
-template <int Q, bool REV = false>
+// U4: 4 blocks per loop trip instead of 2 — ptxas then needs fewer
+// register-shuffling IMAD.MOVs on the FMA-heavy pipe (A/B on B200: 3-4%
+// faster for the 1-Mul kernel up to 8K bits, 3% slower at 32K).
+template <int Q, bool REV = false, bool U4 = false>
 BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_t (&lhcs)[Q + 2]) {
   uint32_t lo[Q], hi[Q], top[Q];
 #pragma unroll
@@ -102,16 +105,47 @@ BN_DEV void conv_chunk(const uint32_t* Ash, const uint32_t* Bsh, int j0, uint32_
   const uint32_t* ap = Ash;
   const uint32_t* bp = Bsh + Q * (j0 - 1);
   int c = j0 + 1;  // blocks left
+  if constexpr (U4) {
 #pragma unroll 1
-  for (; c >= 2; c -= 2) {
-    lds_limbs<Q>(av, ap);
-    lds_limbs<Q>(b1, bp);
-    mac_block<Q>(lo, hi, top, av, b0, b1);
-    lds_limbs<Q>(av, ap + Q);
-    lds_limbs<Q>(b0, bp - Q);
-    mac_block<Q>(lo, hi, top, av, b1, b0);
-    ap += 2 * Q;
-    bp -= 2 * Q;
+    for (; c >= 4; c -= 4) {
+      lds_limbs<Q>(av, ap);
+      lds_limbs<Q>(b1, bp);
+      mac_block<Q>(lo, hi, top, av, b0, b1);
+      lds_limbs<Q>(av, ap + Q);
+      lds_limbs<Q>(b0, bp - Q);
+      mac_block<Q>(lo, hi, top, av, b1, b0);
+      lds_limbs<Q>(av, ap + 2 * Q);
+      lds_limbs<Q>(b1, bp - 2 * Q);
+      mac_block<Q>(lo, hi, top, av, b0, b1);
+      lds_limbs<Q>(av, ap + 3 * Q);
+      lds_limbs<Q>(b0, bp - 3 * Q);
+      mac_block<Q>(lo, hi, top, av, b1, b0);
+      ap += 4 * Q;
+      bp -= 4 * Q;
+    }
+    if (c >= 2) {
+      lds_limbs<Q>(av, ap);
+      lds_limbs<Q>(b1, bp);
+      mac_block<Q>(lo, hi, top, av, b0, b1);
+      lds_limbs<Q>(av, ap + Q);
+      lds_limbs<Q>(b0, bp - Q);
+      mac_block<Q>(lo, hi, top, av, b1, b0);
+      ap += 2 * Q;
+      bp -= 2 * Q;
+      c -= 2;
+    }
+  } else {
+#pragma unroll 1
+    for (; c >= 2; c -= 2) {
+      lds_limbs<Q>(av, ap);
+      lds_limbs<Q>(b1, bp);
+      mac_block<Q>(lo, hi, top, av, b0, b1);
+      lds_limbs<Q>(av, ap + Q);
+      lds_limbs<Q>(b0, bp - Q);
+      mac_block<Q>(lo, hi, top, av, b1, b0);
+      ap += 2 * Q;
+      bp -= 2 * Q;
+    }
   }
   if (c) {
     lds_limbs<Q>(av, ap);
@@ -392,8 +426,8 @@ __global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
     {
       const uint32_t* Ai = As + conv_slot * C::SA;
       const uint32_t* Bi = Bs + conv_slot * C::SB + Q;
-      conv_chunk<Q>(Ai, Bi, g, lh0);
-      conv_chunk<Q>(Ai, Bi, M / Q - 1 - g, lh1);
+      conv_chunk<Q, false, (LOGM <= 8)>(Ai, Bi, g, lh0);
+      conv_chunk<Q, false, (LOGM <= 8)>(Ai, Bi, M / Q - 1 - g, lh1);
     }
     __syncthreads();
 
