@@ -37,6 +37,10 @@ namespace cg = cooperative_groups;
 // (2^18 as a 2 x 512 cluster: 8.76 ms vs 7.37 ms one CTA; 2^19: 10.9 vs 9.6;
 // 2^20: 13.3 vs 12.2), so the defaults are 1024 and one CTA up to 2^18.
 // -DBN_NTT14_CLUSTER -DBN_NTT_CL_T=512 [-DBN_NTT_CL_MINB=1] rebuild the variants.
+// smallest log2 N that uses the 32-element-per-thread kernel
+#ifndef BN_NTT_R32_MIN
+#define BN_NTT_R32_MIN 13
+#endif
 #ifndef BN_NTT_CL_MINB
 #define BN_NTT_CL_MINB 2
 #endif
@@ -108,12 +112,14 @@ struct NttCfg {
 
 // pass P covers forward stages [S0, S1); its 16 register elements are the
 // indices whose bits [LO, LO+4) vary (all other bits come from the thread id).
-template <int LOGN, int P>
-struct PassCfg {
-  static constexpr int S0 = 4 * P;
-  static constexpr int S1 = (4 * P + 4 < LOGN) ? 4 * P + 4 : LOGN;
-  static constexpr int LO = (LOGN - 4 * (P + 1)) > 0 ? LOGN - 4 * (P + 1) : 0;
+template <int LOGN, int P, int RB = 4>
+struct PassCfgR {
+  static constexpr int S0 = RB * P;
+  static constexpr int S1 = (RB * P + RB < LOGN) ? RB * P + RB : LOGN;
+  static constexpr int LO = (LOGN - RB * (P + 1)) > 0 ? LOGN - RB * (P + 1) : 0;
 };
+template <int LOGN, int P>
+using PassCfg = PassCfgR<LOGN, P, 4>;
 
 template <int LO>
 BN_DEV int lay(int t, int e) {
@@ -136,16 +142,16 @@ BN_DEV void bar() {
 // transformed together — every twiddle load serves both, and the two
 // independent dependency chains double the ILP at the register cost the
 // held A-hat used to have).
-template <int LOGN, int P, bool PADDED, int NV>
-BN_DEV void fwd_pass(uint32_t (&x)[NV][16], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
-  using PS = PassCfg<LOGN, P>;
+template <int LOGN, int P, bool PADDED, int NV, int R = 16>
+BN_DEV void fwd_pass(uint32_t (&x)[NV][R], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
+  using PS = PassCfgR<LOGN, P, (R == 32 ? 5 : 4)>;
   const int tlow = t & ((1 << PS::LO) - 1);
 #pragma unroll
   for (int s = PS::S0; s < PS::S1; s++) {
     const int b = (LOGN - 1 - s) - PS::LO;
     const uint2* Ts = tw + ((1 << LOGN) - ((1 << LOGN) >> s)) + tlow;
 #pragma unroll
-    for (int e = 0; e < 16; e++) {
+    for (int e = 0; e < R; e++) {
       if (e & (1 << b)) continue;
       const int el = e & ((1 << b) - 1);
       if (PS::LO == 0 && el == 0) {
@@ -173,16 +179,16 @@ BN_DEV void fwd_pass(uint32_t (&x)[NV][16], int t, const uint2* __restrict__ tw,
   }
 }
 
-template <int LOGN, int P>
-BN_DEV void inv_pass(uint32_t (&x)[16], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
-  using PS = PassCfg<LOGN, P>;
+template <int LOGN, int P, int R = 16>
+BN_DEV void inv_pass(uint32_t (&x)[R], int t, const uint2* __restrict__ tw, uint32_t p, uint32_t p2) {
+  using PS = PassCfgR<LOGN, P, (R == 32 ? 5 : 4)>;
   const int tlow = t & ((1 << PS::LO) - 1);
 #pragma unroll
   for (int s = PS::S1 - 1; s >= PS::S0; s--) {
     const int b = (LOGN - 1 - s) - PS::LO;
     const uint2* Ts = tw + ((1 << LOGN) - ((1 << LOGN) >> s)) + tlow;
 #pragma unroll
-    for (int e = 0; e < 16; e++) {
+    for (int e = 0; e < R; e++) {
       if (e & (1 << b)) continue;
       const int el = e & ((1 << b) - 1);
       if (PS::LO == 0 && el == 0) {  // w^0 = 1
@@ -577,6 +583,174 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
     ntt_product<LOGN, false, false, false, false, true>(sm, slot, t, ai, bi, nullptr, t3, valid, tw);
     ntt_product<LOGN, false, true, true, true, false>(sm, slot, t, t1, t2, t3, out + io, valid, tw);
   }
+}
+
+// ------------------------------------------------------------ 32 elements per thread
+// N = 2^13, 2^14 (128K / 256K bits): T = N / 32 threads (256 / 512) each
+// holding R = 32 register elements, 5 stages per register pass, so a
+// transform is 3 passes / 2 exchanges instead of 4 / 3, and the thread count
+// drops to where up to 128 registers are available (no spills; the 16-element
+// kernel at 1024 threads is capped at 64).  Exchange addresses: element
+// (t, e) of a pass with low bit LO lives at u = lay(t, e) with 5 register
+// bits, swizzled u ^ ((u >> 5) & 31) — for a warp (32 consecutive t, fixed
+// e) the 5 bank bits are a bijection of t's low 5 bits for every LO, so
+// every exchange access is conflict free.  Epilogue: 16 consecutive
+// coefficients per thread (M / T = 16), resolved 16 limbs per thread.
+template <int LOGN>
+struct NttR32Cfg {
+  static constexpr int N = 1 << LOGN, M = N / 2, R = 32, RB = 5;
+  static constexpr int T = N / R;
+  static constexpr int SMEM_WORDS = 2 * N + 3 * M + T / 32;
+  static constexpr int MINB = T <= 256 ? 2 : 1;  // <= 128 registers
+  static_assert((LOGN + RB - 1) / RB == 3, "three register passes");
+};
+
+BN_DEV int swz5(int u) { return u ^ ((u >> 5) & 31); }
+template <int LO>
+BN_DEV int lay32(int t, int e) {
+  return (t & ((1 << LO) - 1)) | (e << LO) | ((t >> LO) << (LO + 5));
+}
+
+template <int LO_FROM, int LO_TO, int NV, int PLANE>
+BN_DEV void xchg32(uint32_t (&x)[NV][32], uint32_t* X0, int t) {
+  __syncthreads();  // previous readers of the planes are done
+  const int bw = swz5(lay32<LO_FROM>(t, 0));
+#pragma unroll
+  for (int v = 0; v < NV; v++)
+#pragma unroll
+    for (int e = 0; e < 32; e++) X0[v * PLANE + (bw ^ swz5(e << LO_FROM))] = x[v][e];
+  __syncthreads();
+  const int br = swz5(lay32<LO_TO>(t, 0));
+#pragma unroll
+  for (int v = 0; v < NV; v++)
+#pragma unroll
+    for (int e = 0; e < 32; e++) x[v][e] = X0[v * PLANE + (br ^ swz5(e << LO_TO))];
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
+    mul_ntt_r32_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                       const uint2* __restrict__ tw) {
+  using C = NttR32Cfg<LOGN>;
+  constexpr int N = C::N, M = C::M, T = C::T;
+  constexpr int L0 = PassCfgR<LOGN, 0, 5>::LO, L1 = PassCfgR<LOGN, 1, 5>::LO, L2 = PassCfgR<LOGN, 2, 5>::LO;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* X = sm;              // plane 0 | plane 1 (N words each)
+  uint32_t* Res = sm + 2 * N;    // 3 M residues
+  uint32_t* agg = Res + 3 * M;   // T / 32
+  const int t = threadIdx.x;
+  for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x) {
+    const uint32_t* ai = a + inst * M;
+    const uint32_t* bi = b + inst * M;
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xab[2][32];
+      // N-1: limbs mod p in pass-0 layout (index t + e N/32), top half zero
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        xab[0][e] = red2(red2(__ldg(ai + t + e * (N / 32)), p2), p2);
+        xab[1][e] = red2(red2(__ldg(bi + t + e * (N / 32)), p2), p2);
+      }
+#pragma unroll
+      for (int e = 16; e < 32; e++) xab[0][e] = xab[1][e] = 0u;
+      // N-2: forward DIF, 3 passes
+      fwd_pass<LOGN, 0, true, 2, 32>(xab, t, twf, p, p2);
+      xchg32<L0, L1, 2, N>(xab, X, t);
+      fwd_pass<LOGN, 1, true, 2, 32>(xab, t, twf, p, p2);
+      xchg32<L1, L2, 2, N>(xab, X, t);
+      fwd_pass<LOGN, 2, true, 2, 32>(xab, t, twf, p, p2);
+      // N-3: pointwise
+      uint32_t x[1][32];
+#pragma unroll
+      for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
+      // N-4: inverse DIT, 3 passes back to the pass-0 layout
+      inv_pass<LOGN, 2, 32>(x[0], t, twi, p, p2);
+      xchg32<L2, L1, 1, N>(x, X, t);
+      inv_pass<LOGN, 1, 32>(x[0], t, twi, p, p2);
+      xchg32<L1, L0, 1, N>(x, X, t);
+      inv_pass<LOGN, 0, 32>(x[0], t, twi, p, p2);
+#pragma unroll
+      for (int e = 0; e < 16; e++) Res[j * M + t + e * (N / 32)] = x[0][e];
+    }
+    __syncthreads();
+
+    // N-5 / N-6: Garner CRT of 16 consecutive coefficients, aggregate, publish
+    {
+      const CrtConst& k = c_crt[LOGN];
+      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+      uint32_t lows[16];
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        uint32_t y0[8], y1[8], y2[8];
+        lds_limbs<8>(y0, Res + 0 * M + 16 * t + 8 * h);
+        lds_limbs<8>(y1, Res + 1 * M + 16 * t + 8 * h);
+        lds_limbs<8>(y2, Res + 2 * M + 16 * t + 8 * h);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+          const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+          const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+          const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+          const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+          const uint32_t d = red2(b2v + c2v, 2 * p2);
+          const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+          const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
+          add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
+          lows[8 * h + q] = a0;
+          a0 = a1;
+          a1 = a2;
+          a2 = 0;
+        }
+      }
+      uint32_t hs[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      uint32_t* L = X;
+      uint32_t* H = X + N;
+      sts_limbs<16>(L + 16 * t, lows);
+      if (16 * t + 16 < M) {
+        sts_limbs<16>(H + 16 * t + 16, hs);
+      } else {
+        uint32_t z[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) z[q] = 0;
+        sts_limbs<16>(H, z);
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t xl[16], yh[16], r[16];
+      lds_limbs<16>(xl, X + 16 * t);
+      lds_limbs<16>(yh, X + N + 16 * t);
+      add_regs<16, T>(xl, yh, r, true, agg);
+      store_limbs<16>(out + inst * M + 16 * t, r);
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_ntt_r32_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                    const NttTables& tb, cudaStream_t st, int n_sm) {
+  using C = NttR32Cfg<LOGN>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  static LaunchCache cache;
+  int per_sm = 0;
+  cudaError_t e = resident_ctas(cache, mul_ntt_r32_kernel<LOGN>, C::T, smem, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;
+  const unsigned grid = cap_grid((unsigned)(n_inst < cap ? n_inst : cap));
+  mul_ntt_r32_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ beyond one CTA
@@ -1070,11 +1244,15 @@ cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uin
     case 8: return launch_ntt_t<8>(out, a, b, n_inst, tb, st, n_sm);
     case 9: return launch_ntt_t<9>(out, a, b, n_inst, tb, st, n_sm);
     case 10: return launch_ntt_t<10>(out, a, b, n_inst, tb, st, n_sm);
-    case 11: return launch_ntt_t<11>(out, a, b, n_inst, tb, st, n_sm);
-    case 12: return launch_ntt_t<12>(out, a, b, n_inst, tb, st, n_sm);
-    case 13: return launch_ntt_t<13>(out, a, b, n_inst, tb, st, n_sm);
+    case 11: return BN_NTT_R32_MIN <= 11 ? launch_ntt_r32_t<11>(out, a, b, n_inst, tb, st, n_sm)
+                                         : launch_ntt_t<11>(out, a, b, n_inst, tb, st, n_sm);
+    case 12: return BN_NTT_R32_MIN <= 12 ? launch_ntt_r32_t<12>(out, a, b, n_inst, tb, st, n_sm)
+                                         : launch_ntt_t<12>(out, a, b, n_inst, tb, st, n_sm);
+    case 13: return BN_NTT_R32_MIN <= 13 ? launch_ntt_r32_t<13>(out, a, b, n_inst, tb, st, n_sm)
+                                         : launch_ntt_t<13>(out, a, b, n_inst, tb, st, n_sm);
 #ifndef BN_NTT14_CLUSTER
-    case 14: return launch_ntt_t<14>(out, a, b, n_inst, tb, st, n_sm);
+    case 14: return BN_NTT_R32_MIN <= 14 ? launch_ntt_r32_t<14>(out, a, b, n_inst, tb, st, n_sm)
+                                         : launch_ntt_t<14>(out, a, b, n_inst, tb, st, n_sm);
 #endif
     default: return cudaErrorInvalidValue;
   }
