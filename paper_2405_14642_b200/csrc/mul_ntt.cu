@@ -991,6 +991,210 @@ static cudaError_t launch_ntt_cluster_t(uint32_t* out, const uint32_t* a, const 
   return cudaGetLastError();
 }
 
+// Cluster version of the 32-element kernel (2^19, 2^20 bits): T = 512
+// threads x 32 elements per CTA, CR = N / 16384 CTAs (2 / 4).  Same
+// structure as mul_ntt_cluster_kernel — only pass 0 <-> 1 crosses CTAs
+// (DSMEM), later exchanges are the local conflict-free xchg32 over the CTA's
+// 2^14-word slice — with 128 registers and one fewer exchange per transform.
+template <int LOGN>
+struct NttCl32Cfg {
+  static constexpr int N = 1 << LOGN, M = N / 2, T = 512, LT = 9;
+  static constexpr int CR = N / (T * 32);
+  static constexpr int PL = T * 32;  // 16384
+  static constexpr int MS = M / CR;  // 8192 = 16 T
+  static constexpr int NP = (LOGN + 4) / 5;
+  static constexpr int SMEM_WORDS = 2 * PL + 3 * MS + T / 32 + 2 * CR;
+  static_assert(CR >= 2 && CR <= 8 && MS == 16 * T, "cluster32 layout");
+  static_assert(PassCfgR<LOGN, 1, 5>::LO <= LT, "rank bits on top from pass 1 on");
+};
+
+template <int LO>
+BN_DEV int unlay32_t(int u) { return (u & ((1 << LO) - 1)) | ((u >> (LO + 5)) << LO); }
+
+template <int LOGN, int LO_FROM, int LO_TO, int NV, class Cluster>
+BN_DEV void xchg_cl32(uint32_t (&x)[NV][32], uint32_t* X0, int gt, Cluster& cl) {
+  using C = NttCl32Cfg<LOGN>;
+  cl.sync();
+  const uint32_t x0 = smem_addr(X0);
+#pragma unroll
+  for (int e = 0; e < 32; e++) {
+    const int u = lay32<LO_FROM>(gt, e);
+    const int gto = unlay32_t<LO_TO>(u);
+    const int eto = (u >> LO_TO) & 31;
+    const uint32_t dst = mapa_rank(x0 + 4 * (eto * C::T + (gto & (C::T - 1))), gto >> C::LT);
+#pragma unroll
+    for (int v = 0; v < NV; v++) st_cluster(dst + 4 * v * C::PL, x[v][e]);
+  }
+  cl.sync();
+#pragma unroll
+  for (int v = 0; v < NV; v++)
+#pragma unroll
+    for (int e = 0; e < 32; e++) x[v][e] = X0[v * C::PL + e * C::T + threadIdx.x];
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(512, 1)
+    mul_ntt_cluster32_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                             const uint2* __restrict__ tw) {
+  using C = NttCl32Cfg<LOGN>;
+  constexpr int N = C::N, M = C::M, MS = C::MS, PL = C::PL;
+  constexpr int L0 = PassCfgR<LOGN, 0, 5>::LO, L1 = PassCfgR<LOGN, 1, 5>::LO, L2 = PassCfgR<LOGN, 2, 5>::LO;
+  constexpr int L3 = PassCfgR<LOGN, 3, 5>::LO;
+  extern __shared__ __align__(16) uint32_t sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const int gt = rank * C::T + tid;
+  uint32_t* X0 = sm;
+  uint32_t* Res = sm + 2 * PL;
+  uint32_t* agg = Res + 3 * MS;
+  uint32_t* cta_agg = agg + C::T / 32;
+  const uint64_t n_cl = gridDim.x / C::CR;
+  int parity = 0;
+  for (uint64_t inst = blockIdx.x / C::CR; inst < n_inst; inst += n_cl, parity ^= 1) {
+    const uint32_t* ai = a + inst * M;
+    const uint32_t* bi = b + inst * M;
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xab[2][32];
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        xab[0][e] = red2(red2(__ldg(ai + gt + e * (N / 32)), p2), p2);
+        xab[1][e] = red2(red2(__ldg(bi + gt + e * (N / 32)), p2), p2);
+      }
+#pragma unroll
+      for (int e = 16; e < 32; e++) xab[0][e] = xab[1][e] = 0u;
+      fwd_pass<LOGN, 0, true, 2, 32>(xab, gt, twf, p, p2);
+      xchg_cl32<LOGN, L0, L1, 2>(xab, X0, gt, cl);
+      fwd_pass<LOGN, 1, true, 2, 32>(xab, gt, twf, p, p2);
+      xchg32<L1, L2, 2, PL>(xab, X0, tid);
+      fwd_pass<LOGN, 2, true, 2, 32>(xab, gt, twf, p, p2);
+      if constexpr (C::NP > 3) {
+        xchg32<L2, L3, 2, PL>(xab, X0, tid);
+        fwd_pass<LOGN, 3, true, 2, 32>(xab, gt, twf, p, p2);
+      }
+      uint32_t x[1][32];
+#pragma unroll
+      for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
+      if constexpr (C::NP > 3) {
+        inv_pass<LOGN, 3, 32>(x[0], gt, twi, p, p2);
+        xchg32<L3, L2, 1, PL>(x, X0, tid);
+      }
+      inv_pass<LOGN, 2, 32>(x[0], gt, twi, p, p2);
+      xchg32<L2, L1, 1, PL>(x, X0, tid);
+      inv_pass<LOGN, 1, 32>(x[0], gt, twi, p, p2);
+      xchg_cl32<LOGN, L1, L0, 1>(x, X0, gt, cl);
+      inv_pass<LOGN, 0, 32>(x[0], gt, twi, p, p2);
+      // coefficient k = gt + e N/32 (e < 16) -> its owner's residue array
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        const int k = gt + e * (N / 32);
+        st_cluster(mapa_rank(smem_addr(Res + j * MS + (k & (MS - 1))), k / MS), x[0][e]);
+      }
+    }
+    cl.sync();
+    // CRT / aggregate 16 consecutive coefficients [rank MS + 16 tid, +16)
+    {
+      const CrtConst& k = c_crt[LOGN];
+      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+      uint32_t lows[16];
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        uint32_t y0[8], y1[8], y2[8];
+        lds_limbs<8>(y0, Res + 0 * MS + 16 * tid + 8 * h);
+        lds_limbs<8>(y1, Res + 1 * MS + 16 * tid + 8 * h);
+        lds_limbs<8>(y2, Res + 2 * MS + 16 * tid + 8 * h);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+          const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+          const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+          const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+          const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+          const uint32_t d = red2(b2v + c2v, 2 * p2);
+          const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+          const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
+          add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
+          lows[8 * h + q] = a0;
+          a0 = a1;
+          a1 = a2;
+          a2 = 0;
+        }
+      }
+      uint32_t hs[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      uint32_t* L = X0;
+      uint32_t* H = X0 + PL;
+      sts_limbs<16>(L + 16 * tid, lows);
+      if (tid < C::T - 1) {
+        sts_limbs<16>(H + 16 * tid + 16, hs);
+      } else {
+        if (rank == C::CR - 1) {
+#pragma unroll
+          for (int q = 0; q < 16; q++) hs[q] = 0;
+        }
+        const uint32_t dst = mapa_rank(smem_addr(H), (rank + 1) % C::CR);
+#pragma unroll
+        for (int q = 0; q < 16; q++) st_cluster(dst + 4 * q, hs[q]);
+      }
+    }
+    cl.sync();
+    {
+      uint32_t xl[16], yh[16], r[16], g, pp;
+      lds_limbs<16>(xl, X0 + 16 * tid);
+      lds_limbs<16>(yh, X0 + PL + 16 * tid);
+      chunk_sum<16>(xl, yh, r, g, pp);
+      const uint32_t cin = cluster_carry_scan<C::CR>(g, pp, agg, cta_agg, parity, cl);
+      chunk_apply<16>(xl, r, cin);
+      store_limbs<16>(out + inst * M + (uint64_t)rank * MS + 16 * tid, r);
+    }
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_ntt_cluster32_t(uint32_t* out, const uint32_t* a, const uint32_t* b,
+                                          uint64_t n_inst, const NttTables& tb, cudaStream_t st) {
+  using C = NttCl32Cfg<LOGN>;
+  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CR;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(C::CR);
+  static LaunchCache cache;
+  int max_cl = 0;
+  cudaError_t e = cached_query(cache, [&](int* o) {
+    cudaError_t e1 = cudaFuncSetAttribute(mul_ntt_cluster32_kernel<LOGN>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e1 != cudaSuccess) return e1;
+    return cudaOccupancyMaxActiveClusters(o, mul_ntt_cluster32_kernel<LOGN>, &cfg);
+  }, &max_cl);
+  if (e != cudaSuccess) return e;
+  if (max_cl < 1) return cudaErrorInvalidConfiguration;
+  uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
+  n_cl = cap_grid((unsigned)n_cl);
+  cfg.gridDim = dim3((unsigned)(n_cl * C::CR));
+  e = cudaLaunchKernelEx(&cfg, mul_ntt_cluster32_kernel<LOGN>, out, a, b, n_inst, tb.tw);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ full product
 // Wide (untruncated) product: out[k] = a[k] * b[k] as 2m
 // limbs.  The N = 2m point transform already yields every coefficient
@@ -1237,8 +1441,14 @@ cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uin
 #ifdef BN_NTT14_CLUSTER
     case 14: return launch_ntt_cluster_t<14, 512>(out, a, b, n_inst, tb, st, n_sm);
 #endif
+#ifndef BN_NTT_CL16
+    // 32 elements per thread (A/B: 2^19 9.55 -> 8.30 ms, 2^20 12.1 -> 11.5 ms)
+    case 15: return launch_ntt_cluster32_t<15>(out, a, b, n_inst, tb, st);
+    case 16: return launch_ntt_cluster32_t<16>(out, a, b, n_inst, tb, st);
+#else
     case 15: return launch_ntt_cluster_t<15, BN_NTT_CL_T>(out, a, b, n_inst, tb, st, n_sm);
     case 16: return launch_ntt_cluster_t<16, BN_NTT_CL_T>(out, a, b, n_inst, tb, st, n_sm);
+#endif
     case 6: return launch_ntt_t<6>(out, a, b, n_inst, tb, st, n_sm);
     case 7: return launch_ntt_t<7>(out, a, b, n_inst, tb, st, n_sm);
     case 8: return launch_ntt_t<8>(out, a, b, n_inst, tb, st, n_sm);
