@@ -1435,6 +1435,14 @@ static cudaError_t launch_dbg_t(uint32_t* x, uint64_t n_inst, int prime, const N
   return cudaGetLastError();
 }
 
+// 16- or 32-element kernel by size (only the chosen one is instantiated)
+template <int LOGN>
+static cudaError_t launch_ntt_any_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                   const NttTables& tb, cudaStream_t st, int n_sm) {
+  if constexpr (LOGN >= BN_NTT_R32_MIN) return launch_ntt_r32_t<LOGN>(out, a, b, n_inst, tb, st, n_sm);
+  else return launch_ntt_t<LOGN>(out, a, b, n_inst, tb, st, n_sm);
+}
+
 cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                            uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm) {
   switch (logm + 1) {
@@ -1454,15 +1462,11 @@ cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uin
     case 8: return launch_ntt_t<8>(out, a, b, n_inst, tb, st, n_sm);
     case 9: return launch_ntt_t<9>(out, a, b, n_inst, tb, st, n_sm);
     case 10: return launch_ntt_t<10>(out, a, b, n_inst, tb, st, n_sm);
-    case 11: return BN_NTT_R32_MIN <= 11 ? launch_ntt_r32_t<11>(out, a, b, n_inst, tb, st, n_sm)
-                                         : launch_ntt_t<11>(out, a, b, n_inst, tb, st, n_sm);
-    case 12: return BN_NTT_R32_MIN <= 12 ? launch_ntt_r32_t<12>(out, a, b, n_inst, tb, st, n_sm)
-                                         : launch_ntt_t<12>(out, a, b, n_inst, tb, st, n_sm);
-    case 13: return BN_NTT_R32_MIN <= 13 ? launch_ntt_r32_t<13>(out, a, b, n_inst, tb, st, n_sm)
-                                         : launch_ntt_t<13>(out, a, b, n_inst, tb, st, n_sm);
+    case 11: return launch_ntt_any_t<11>(out, a, b, n_inst, tb, st, n_sm);
+    case 12: return launch_ntt_any_t<12>(out, a, b, n_inst, tb, st, n_sm);
+    case 13: return launch_ntt_any_t<13>(out, a, b, n_inst, tb, st, n_sm);
 #ifndef BN_NTT14_CLUSTER
-    case 14: return BN_NTT_R32_MIN <= 14 ? launch_ntt_r32_t<14>(out, a, b, n_inst, tb, st, n_sm)
-                                         : launch_ntt_t<14>(out, a, b, n_inst, tb, st, n_sm);
+    case 14: return launch_ntt_any_t<14>(out, a, b, n_inst, tb, st, n_sm);
 #endif
     default: return cudaErrorInvalidValue;
   }
