@@ -31,8 +31,8 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef BN_CLASSICAL_MINB
-#define BN_CLASSICAL_MINB 2  // 2 x 512-thread CTAs per SM (64 registers)
+#ifndef BN_CLASSICAL_TT
+#define BN_CLASSICAL_TT 0  // 0: per-size default (MulCCfg); else a fixed target CTA size
 #endif
 
 namespace bn {
@@ -51,9 +51,13 @@ struct MulCCfg {
   static constexpr int Q = Q_;
   static constexpr int G = M / (2 * Q);  // column-group threads per instance
   // instances interleaved across warp lanes (keeps trip counts uniform)
-  static constexpr int I = (512 / G) >= 32 ? 32 : ((512 / G) < 1 ? 1 : 512 / G);
+  // target threads per CTA: 256 up to 2K bits (more, smaller CTAs overlap
+  // one group's barriers / epilogue with another's convolution: -9% at 1K,
+  // -4% at 2K by A/B), 512 above (256 is 10% slower at 4K)
+  static constexpr int TT = BN_CLASSICAL_TT > 0 ? BN_CLASSICAL_TT : (LOGM <= 6 ? 256 : 512);
+  static constexpr int I = (TT / G) >= 32 ? 32 : ((TT / G) < 1 ? 1 : TT / G);
   static constexpr int SET_T = I * G;                         // threads per instance set
-  static constexpr int SETS = SET_T >= 512 ? 1 : 512 / SET_T;  // sets per CTA
+  static constexpr int SETS = SET_T >= TT ? 1 : TT / SET_T;   // sets per CTA
   static constexpr int T = SETS * SET_T;                       // threads per CTA
   static constexpr int IPB = SETS * I;                         // instances per CTA
   static constexpr int SA = M + 4;  // A stride: SA/4 odd -> broadcast A loads of <= 8 instances hit distinct banks
@@ -63,7 +67,7 @@ struct MulCCfg {
   static constexpr int SB = M + Q + (((4 * BS - Q) % 32) + 32) % 32;
   static constexpr int STAGE_WORDS = IPB * (SA + SB);      // one group's A and B
   static constexpr int SMEM_WORDS = 2 * STAGE_WORDS + T / 32;  // double-buffered
-  static constexpr int MINB = T >= 1024 ? 1 : BN_CLASSICAL_MINB;  // target residency
+  static constexpr int MINB = T >= 1024 ? 1 : 1024 / T;  // target residency: 64 registers
   static_assert(Q >= 2 && (Q % 4) == 0, "Q must be a multiple of 4 (>= 2 for the L/H layout)");
   static_assert(G >= 1, "size too small for Q");
 };
