@@ -37,6 +37,12 @@ namespace cg = cooperative_groups;
 // (2^18 as a 2 x 512 cluster: 8.76 ms vs 7.37 ms one CTA; 2^19: 10.9 vs 9.6;
 // 2^20: 13.3 vs 12.2), so the defaults are 1024 and one CTA up to 2^18.
 // -DBN_NTT14_CLUSTER -DBN_NTT_CL_T=512 [-DBN_NTT_CL_MINB=1] rebuild the variants.
+// target CTA size of the 16-element kernel for N <= 256 (several instances per CTA)
+#ifndef BN_NTT_TT
+#define BN_NTT_TT 64  // A/B at 4K: 256 -> 2.953 ms, 128 -> 2.879, 64 -> 2.873
+#endif
+// the Poly kernel keeps 256-thread CTAs (64 measured 26% slower for it)
+constexpr int kPolyNttTT = 256;
 // smallest log2 N that uses the 32-element-per-thread kernel
 #ifndef BN_NTT_R32_MIN
 #define BN_NTT_R32_MIN 13
@@ -91,14 +97,15 @@ BN_DEV void ct_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p, uint32_t p2) 
 }
 
 // ------------------------------------------------------------ layout
-template <int LOGN>
+template <int LOGN, int TTA = BN_NTT_TT>
 struct NttCfg {
   static constexpr int N = 1 << LOGN;
   static constexpr int M = N / 2;
   static constexpr int R = 16;
   static constexpr int TPI = N / R;
   static constexpr int NP = (LOGN + 3) / 4;  // register passes
-  static constexpr int IPB = TPI >= 256 ? 1 : 256 / TPI;
+  static constexpr int TT = LOGN <= 8 ? TTA : 256;  // target threads per CTA
+  static constexpr int IPB = TPI >= TT ? 1 : TT / TPI;
   static constexpr int T = IPB * TPI;
   // exchange area (padded by 1/16 for LOGN <= 8, see xbase), raw residues, agg
   static constexpr int XW = LOGN <= 8 ? IPB * N + (IPB * N >> 4) : IPB * N;
@@ -107,7 +114,7 @@ struct NttCfg {
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
   // (A/B on B200: best of {3,4} x {2,3} for T = 256; 2 for T = 512; T = 1024
   // must keep 64 registers)
-  static constexpr int MINB = T <= 256 ? (LOGN <= 8 ? 3 : 2) : (T == 512 ? 2 : 1);
+  static constexpr int MINB = LOGN <= 8 ? (768 / T > 1 ? 768 / T : 1) : (T <= 256 ? 2 : (T == 512 ? 2 : 1));
 };
 
 // pass P covers forward stages [S0, S1); its 16 register elements are the
@@ -249,10 +256,10 @@ BN_DEV void xchg(uint32_t (&x)[NV][16], uint32_t* X0, int xo, int t) {
     for (int e = 0; e < 16; e++) x[v][e] = X0[v * PLANE + xaddr<LOGN, LO_TO>(br, e)];
 }
 
-template <int LOGN, bool PADDED, int NV>
+template <int LOGN, bool PADDED, int NV, int TTA = BN_NTT_TT>
 BN_DEV void fwd_all(uint32_t (&x)[NV][16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p,
                     uint32_t p2) {
-  using C = NttCfg<LOGN>;
+  using C = NttCfg<LOGN, TTA>;
   constexpr int PL = C::XW;
   fwd_pass<LOGN, 0, PADDED, NV>(x, t, tw, p, p2);
   if constexpr (C::NP > 1) {
@@ -270,9 +277,9 @@ BN_DEV void fwd_all(uint32_t (&x)[NV][16], uint32_t* X0, int xo, int t, const ui
   static_assert(C::NP <= 4, "LOGN <= 16");
 }
 
-template <int LOGN>
+template <int LOGN, int TTA = BN_NTT_TT>
 BN_DEV void inv_all(uint32_t (&x1)[16], uint32_t* X0, int xo, int t, const uint2* tw, uint32_t p, uint32_t p2) {
-  using C = NttCfg<LOGN>;
+  using C = NttCfg<LOGN, TTA>;
   constexpr int PL = C::XW;
   uint32_t(&x)[1][16] = reinterpret_cast<uint32_t(&)[1][16]>(x1);
   if constexpr (C::NP > 3) {
@@ -305,10 +312,10 @@ BN_DEV void add3(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t c0, uint32_t
 // XWS / AWS / OWS: operand / addend / destination live in the in-kernel
 // workspace (coherent ld.global.cg, write-back stores) instead of HBM
 // (ld.global.nc, streaming stores).  Ends with a CTA barrier.
-template <int LOGN, bool SQ, bool ADD, bool XWS, bool AWS, bool OWS>
+template <int LOGN, bool SQ, bool ADD, bool XWS, bool AWS, bool OWS, int TTA = kPolyNttTT>
 BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const uint32_t* yi,
                         const uint32_t* addi, uint32_t* dsti, bool valid, const uint2* __restrict__ tw) {
-  using C = NttCfg<LOGN>;
+  using C = NttCfg<LOGN, TTA>;
   constexpr int N = C::N, M = C::M, TPI = C::TPI;
   // this slot's own (padded) exchange region, reused for L | H after the
   // transforms: it must not reach into another slot's region, because slots
@@ -347,13 +354,13 @@ BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const
       for (int v = 0; v < NV; v++) xab[v][e] = 0u;
     }
     // N-2: forward transforms of x and y together (one when squaring)
-    fwd_all<LOGN, true, NV>(xab, sm, slot * N, t, twf, p, p2);
+    fwd_all<LOGN, true, NV, TTA>(xab, sm, slot * N, t, twf, p, p2);
     // N-3: pointwise product (same register layout for both transforms)
     uint32_t x[16];
 #pragma unroll
     for (int e = 0; e < 16; e++) x[e] = mont(xab[0][e], xab[NV - 1][e], p, pinv);
     // N-4: inverse transform -> pass-0 layout, natural order
-    inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
+    inv_all<LOGN, TTA>(x, sm, slot * N, t, twi, p, p2);
     // keep coefficients 0..M-1 (truncated product): e < 8
 #pragma unroll
     for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
@@ -559,10 +566,10 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
 // to this CTA's private workspace slice (L2-resident, rewritten by the same
 // CTA group after group) and are read back coherently by the last product.
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
+__global__ void __launch_bounds__(NttCfg<LOGN, kPolyNttTT>::T, NttCfg<LOGN, kPolyNttTT>::MINB)
     poly_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                     const uint2* __restrict__ tw, uint32_t* ws) {
-  using C = NttCfg<LOGN>;
+  using C = NttCfg<LOGN, kPolyNttTT>;
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   const int slot = threadIdx.x / C::TPI;
@@ -1392,7 +1399,7 @@ static cudaError_t launch_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t
 
 template <int LOGN>
 static cudaError_t poly_ntt_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64_t* ws_words) {
-  using C = NttCfg<LOGN>;
+  using C = NttCfg<LOGN, kPolyNttTT>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
   static LaunchCache cache;
   int per_sm = 0;
@@ -1410,7 +1417,7 @@ template <int LOGN>
 static cudaError_t launch_poly_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                      const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
                                      int n_sm) {
-  using C = NttCfg<LOGN>;
+  using C = NttCfg<LOGN, kPolyNttTT>;
   unsigned grid = 0;
   uint64_t need = 0;
   cudaError_t e = poly_ntt_geom_t<LOGN>(n_inst, n_sm, &grid, &need);
