@@ -41,6 +41,9 @@ namespace cg = cooperative_groups;
 #ifndef BN_NTT_TT
 #define BN_NTT_TT 64  // A/B at 4K: 256 -> 2.953 ms, 128 -> 2.879, 64 -> 2.873
 #endif
+#ifndef BN_NTT_TT_MAXLOG
+#define BN_NTT_TT_MAXLOG 12  // A/B: 16K -9.4%, 32K -7.7% vs 256-thread CTAs
+#endif
 // the Poly kernel keeps 256-thread CTAs (64 measured 26% slower for it)
 constexpr int kPolyNttTT = 256;
 // smallest log2 N that uses the 32-element-per-thread kernel
@@ -104,7 +107,7 @@ struct NttCfg {
   static constexpr int R = 16;
   static constexpr int TPI = N / R;
   static constexpr int NP = (LOGN + 3) / 4;  // register passes
-  static constexpr int TT = LOGN <= 8 ? TTA : 256;  // target threads per CTA
+  static constexpr int TT = LOGN <= BN_NTT_TT_MAXLOG ? TTA : 256;  // target threads per CTA
   static constexpr int IPB = TPI >= TT ? 1 : TT / TPI;
   static constexpr int T = IPB * TPI;
   // exchange area (padded by 1/16 for LOGN <= 8, see xbase), raw residues, agg
@@ -114,7 +117,8 @@ struct NttCfg {
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
   // (A/B on B200: best of {3,4} x {2,3} for T = 256; 2 for T = 512; T = 1024
   // must keep 64 registers)
-  static constexpr int MINB = LOGN <= 8 ? (768 / T > 1 ? 768 / T : 1) : (T <= 256 ? 2 : (T == 512 ? 2 : 1));
+  static constexpr int MINB = LOGN <= 8 ? (768 / T > 1 ? 768 / T : 1)
+                                        : (T <= 256 ? (512 / T > 1 ? 512 / T : 1) : (T == 512 ? 2 : 1));
 };
 
 // pass P covers forward stages [S0, S1); its 16 register elements are the
