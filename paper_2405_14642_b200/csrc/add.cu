@@ -24,6 +24,12 @@ namespace cg = cooperative_groups;
 #ifndef BN_ADD_CL_STAGES
 #define BN_ADD_CL_STAGES 2  // cp.async stages of the cluster add (64 KiB each; 3 measured no faster)
 #endif
+#ifndef BN_ADD6_L_LOGM10
+#define BN_ADD6_L_LOGM10 8
+#endif
+#ifndef BN_ADD6_L_LOGM11
+#define BN_ADD6_L_LOGM11 8
+#endif
 
 namespace bn {
 
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
     const uint64_t inst = grp * C::IPB + slot;
     const bool valid = inst < n_inst;
     const uint64_t off = inst * (uint64_t)C::M + (uint64_t)lt * L;
-    uint32_t x[L], y[L], r[L], s[L];
+    uint32_t x[L], y[L], r[L];
     if (valid) {
       load_limbs<L>(x, a + off);
       load_limbs<L>(y, b + off);
@@ -91,12 +97,12 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
       for (int i = 0; i < L; i++) x[i] = y[i] = 0;
     }
     add_regs<L, C::TPI>(x, y, r, valid, agg[0]);  // a + b
-    add_regs<L, C::TPI>(r, x, s, valid, agg[1]);  // + a
-    add_regs<L, C::TPI>(s, y, r, valid, agg[0]);  // + b
-    add_regs<L, C::TPI>(r, x, s, valid, agg[1]);  // + a
-    add_regs<L, C::TPI>(s, y, r, valid, agg[0]);  // + b
-    add_regs<L, C::TPI>(r, x, s, valid, agg[1]);  // + a
-    if (valid) store_limbs<L>(out + off, s);
+    add_regs_inplace<L, C::TPI>(r, x, valid, agg[1]);  // + a
+    add_regs_inplace<L, C::TPI>(r, y, valid, agg[0]);  // + b
+    add_regs_inplace<L, C::TPI>(r, x, valid, agg[1]);  // + a
+    add_regs_inplace<L, C::TPI>(r, y, valid, agg[0]);  // + b
+    add_regs_inplace<L, C::TPI>(r, x, valid, agg[1]);  // + a
+    if (valid) store_limbs<L>(out + off, r);
     if constexpr (C::TPI > 32) __syncthreads();
   }
 }
@@ -196,10 +202,21 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   return cudaGetLastError();
 }
 
+// 6-Add limbs per thread (A/B on one box, ms per paper batch): L = 8 up to
+// 8K bits (one warp per instance); 16K: L = 16 (TPI = 32, no CTA barrier:
+// 0.335 -> 0.264 ms); 32K / 64K: L = 8 (L = 16: 0.324 -> 0.386, L = 32:
+// 0.445); 128K / 256K: L = 16 (at L = 8, 40 registers x 1024 threads left
+// one CTA per SM: 128K 0.370 -> 0.342, 256K 0.555 -> 0.377 ms).  Parking a
+// and b in shared memory (32 registers) and a cp.async double-buffered
+// persistent variant both measured slower (256K 0.435 / 0.586 ms).
+constexpr int add6_limbs_per_thread(int logm) {
+  return logm <= 8 ? 8 : logm == 10 ? BN_ADD6_L_LOGM10 : logm == 11 ? BN_ADD6_L_LOGM11 : 16;
+}
+
 template <int LOGM>
 static cudaError_t launch_add6_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                  cudaStream_t st, int n_sm) {
-  constexpr int L = 8;
+  constexpr int L = add6_limbs_per_thread(LOGM);
   using C = AddCfg<LOGM, L>;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   const uint64_t per_sm = 2048 / C::BLOCK;

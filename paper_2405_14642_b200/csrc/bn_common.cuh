@@ -298,4 +298,15 @@ BN_DEV void add_regs(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&
   chunk_apply<L>(x, r, cin);
 }
 
+// r += y in place (the fused 6-Add accumulator: one limb set fewer live
+// than add_regs).
+template <int L, int TPI>
+BN_DEV void add_regs_inplace(uint32_t (&r)[L], const uint32_t (&y)[L], bool valid, uint32_t* agg) {
+  uint32_t g, p;
+  chunk_sum<L>(r, y, r, g, p);
+  if (!valid) g = p = 0;
+  uint32_t cin = carry_scan<TPI>(g, p, agg);
+  chunk_apply<L>(y, r, cin);
+}
+
 }  // namespace bn
