@@ -24,6 +24,13 @@ namespace cg = cooperative_groups;
 #ifndef BN_ADD_CL_STAGES
 #define BN_ADD_CL_STAGES 2  // cp.async stages of the cluster add (64 KiB each; 3 measured no faster)
 #endif
+// add at 2^19 / 2^20 bits (A/B on B200, ms per paper batch; 512K / 1M):
+//   0: 1024-thread clusters of 2 / 4 CTAs, 8 limbs, cp.async staging, 1 CTA/SM: 0.402 / 0.490
+//   1: one CTA x 16 limbs (512K); 2-CTA cluster x 16 limbs, direct loads (1M): 0.331 / 0.379
+//   2: clusters of 2 / 4 CTAs, 8 limbs, direct loads, 32 registers, 2 CTAs/SM: 0.310 / 0.336
+#ifndef BN_ADD_BIG
+#define BN_ADD_BIG 2
+#endif
 #ifndef BN_ADD6_L_LOGM10
 #define BN_ADD6_L_LOGM10 8
 #endif
@@ -108,23 +115,23 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
 }
 
 // Sizes beyond one CTA (2^19, 2^20 bits): one instance per
-// thread-block cluster of CR = M / 8192 CTAs (2 or 4), CTA rank r holding
-// limbs [r M/CR, (r+1) M/CR), 1024 threads x 8 limbs.  The carry scan runs
+// thread-block cluster of CR = M / (1024 L) CTAs, CTA rank r holding
+// limbs [r M/CR, (r+1) M/CR), 1024 threads x L limbs.  The carry scan runs
 // across the cluster (cluster_carry_scan: the CTA aggregates travel through
 // DSMEM) — the hierarchical scan of PAPER.md:289-292 with one more level,
 // instead of the single-pass decoupled look-back over global memory the
 // paper cites.
-// Each thread stages the next NS - 1 instances' 2 x 8 limbs into shared
-// memory with cp.async (NS stages of 64 KiB per CTA) while it scans and
-// stores the current one, so HBM reads stay in flight across the cluster
-// barriers; a thread only ever reads back what it copied itself (no CTA
-// barrier needed).
-template <int LOGM>
-__global__ void __launch_bounds__(1024, 1)
+// NS > 0: each thread stages the next NS - 1 instances' 2 x L limbs into
+// shared memory with cp.async (NS stages of 64 KiB per CTA) while it scans
+// and stores the current one; a thread only ever reads back what it copied
+// itself (no CTA barrier needed).  NS = 0: limbs are loaded straight into
+// registers, and with MB = 2 (32 registers) two clusters share each SM so
+// one's loads overlap the other's cluster barrier — the default (BN_ADD_BIG).
+template <int LOGM, int L, int NS, int MB>
+__global__ void __launch_bounds__(1024, MB)
     add_cluster_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
                        const uint32_t* __restrict__ b, uint64_t n_inst) {
-  constexpr int M = 1 << LOGM, L = 8, CR = M / (1024 * L), SL = M / CR;  // limbs per CTA
-  constexpr int NS = BN_ADD_CL_STAGES;            // instances in flight + 1
+  constexpr int M = 1 << LOGM, CR = M / (1024 * L), SL = M / CR;  // limbs per CTA
   extern __shared__ __align__(16) uint32_t sm[];  // [NS stages][a | b][SL]
   __shared__ uint32_t agg[32];
   __shared__ uint32_t cta_agg[2 * CR];
@@ -149,28 +156,34 @@ __global__ void __launch_bounds__(1024, 1)
     cp_async_commit();
   }
   int parity = 0;
-  for (int st = 0; inst < n_inst; inst += n_cl, parity ^= 1, st = st == NS - 1 ? 0 : st + 1) {
-    const int sf = st == 0 ? NS - 1 : st - 1;  // stage of instance inst + (NS-1) n_cl
-    if (inst + (NS - 1) * n_cl < n_inst) stage(inst + (NS - 1) * n_cl, sf);
-    cp_async_commit();
-    cp_async_wait<NS - 1>();
+  for (int st = 0; inst < n_inst; inst += n_cl, parity ^= 1, st = st >= NS - 1 ? 0 : st + 1) {
     uint32_t x[L], y[L], r[L], g, p;
-    lds_limbs<L>(x, sm + st * 2 * SL + lo);
-    lds_limbs<L>(y, sm + st * 2 * SL + SL + lo);
+    const uint64_t off = inst * (uint64_t)M + (uint64_t)rank * SL + lo;
+    if constexpr (NS > 0) {
+      const int sf = st == 0 ? NS - 1 : st - 1;  // stage of instance inst + (NS-1) n_cl
+      if (inst + (NS - 1) * n_cl < n_inst) stage(inst + (NS - 1) * n_cl, sf);
+      cp_async_commit();
+      cp_async_wait<NS - 1>();
+      lds_limbs<L>(x, sm + st * 2 * SL + lo);
+      lds_limbs<L>(y, sm + st * 2 * SL + SL + lo);
+    } else {
+      load_limbs<L>(x, a + off);
+      load_limbs<L>(y, b + off);
+    }
     chunk_sum<L>(x, y, r, g, p);
     const uint32_t cin = cluster_carry_scan<CR>(g, p, agg, cta_agg, parity, cl);
     chunk_apply<L>(x, r, cin);
-    store_limbs<L>(out + inst * (uint64_t)M + (uint64_t)rank * SL + lo, r);
+    store_limbs<L>(out + off, r);
   }
-  cp_async_wait<0>();
+  if constexpr (NS > 0) cp_async_wait<0>();
 }
 
-template <int LOGM>
+template <int LOGM, int L = 8, int NS = BN_ADD_CL_STAGES, int MB = 1>
 static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                         cudaStream_t st, int n_sm) {
-  constexpr int CR = (1 << LOGM) / 8192;
+  constexpr int CR = (1 << LOGM) / (1024 * L);
   cudaLaunchConfig_t cfg = {};
-  constexpr size_t smem = BN_ADD_CL_STAGES * 2 * ((1 << LOGM) / CR) * sizeof(uint32_t);
+  constexpr size_t smem = NS * 2 * ((1 << LOGM) / CR) * sizeof(uint32_t);
   cfg.gridDim = dim3(CR);
   cfg.blockDim = dim3(1024);
   cfg.dynamicSmemBytes = smem;
@@ -188,16 +201,16 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   static LaunchCache cache;
   int max_cl = 0;
   cudaError_t e = cached_query(cache, [&](int* o) {
-    cudaError_t e1 = cudaFuncSetAttribute(add_cluster_kernel<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e1 = cudaFuncSetAttribute(add_cluster_kernel<LOGM, L, NS, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e1 != cudaSuccess) return e1;
-    return cudaOccupancyMaxActiveClusters(o, add_cluster_kernel<LOGM>, &cfg);
+    return cudaOccupancyMaxActiveClusters(o, add_cluster_kernel<LOGM, L, NS, MB>, &cfg);
   }, &max_cl);
   if (e != cudaSuccess) return e;
   if (max_cl < 1) return cudaErrorInvalidConfiguration;
   uint64_t n_cl = n_inst < (uint64_t)max_cl ? n_inst : (uint64_t)max_cl;
   n_cl = cap_grid((unsigned)n_cl);
   cfg.gridDim = dim3((unsigned)(n_cl * CR));
-  e = cudaLaunchKernelEx(&cfg, add_cluster_kernel<LOGM>, out, a, b, n_inst);
+  e = cudaLaunchKernelEx(&cfg, add_cluster_kernel<LOGM, L, NS, MB>, out, a, b, n_inst);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -226,10 +239,9 @@ static cudaError_t launch_add6_t(uint32_t* out, const uint32_t* a, const uint32_
   return cudaGetLastError();
 }
 
-template <int LOGM>
+template <int LOGM, int L = 8>
 static cudaError_t launch_add_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                 cudaStream_t st, int n_sm) {
-  constexpr int L = 8;
   using C = AddCfg<LOGM, L>;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   // resident CTAs per SM for this block size (2048 threads/SM)
@@ -243,8 +255,19 @@ static cudaError_t launch_add_t(uint32_t* out, const uint32_t* a, const uint32_t
 cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                        cudaStream_t st, int n_sm) {
   switch (logm) {
+    // 2^19 on one CTA (1024 threads x 16 limbs, 38 registers): 0.402 ms
+    // (2-CTA cluster, 8 limbs) -> 0.329 ms by A/B; 2^20 on a 2-CTA cluster
+    // with 16 limbs per thread, loaded straight into registers
+#if BN_ADD_BIG == 1
+    case 14: return launch_add_t<14, 16>(out, a, b, n_inst, st, n_sm);
+    case 15: return launch_add_cluster_t<15, 16, 0>(out, a, b, n_inst, st, n_sm);
+#elif BN_ADD_BIG == 2
+    case 14: return launch_add_cluster_t<14, 8, 0, 2>(out, a, b, n_inst, st, n_sm);
+    case 15: return launch_add_cluster_t<15, 8, 0, 2>(out, a, b, n_inst, st, n_sm);
+#else
     case 14: return launch_add_cluster_t<14>(out, a, b, n_inst, st, n_sm);
     case 15: return launch_add_cluster_t<15>(out, a, b, n_inst, st, n_sm);
+#endif
     case 5: return launch_add_t<5>(out, a, b, n_inst, st, n_sm);
     case 6: return launch_add_t<6>(out, a, b, n_inst, st, n_sm);
     case 7: return launch_add_t<7>(out, a, b, n_inst, st, n_sm);

@@ -31,6 +31,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef BN_CLASSICAL_2K_MINB
+#define BN_CLASSICAL_2K_MINB 6  // residency target of the 2K-bit 1-Mul kernel
+#endif
 #ifndef BN_CLASSICAL_TT
 #define BN_CLASSICAL_TT 0  // 0: per-size default (MulCCfg); else a fixed target CTA size
 #endif
@@ -68,6 +71,10 @@ struct MulCCfg {
   static constexpr int STAGE_WORDS = IPB * (SA + SB);      // one group's A and B
   static constexpr int SMEM_WORDS = 2 * STAGE_WORDS + T / 32;  // double-buffered
   static constexpr int MINB = T >= 1024 ? 1 : 1024 / T;  // target residency: 64 registers
+  // the 1-Mul kernel at 2K bits: 6 CTAs (40 registers, no spills) by A/B
+  // 0.777 -> 0.748 ms; at 1K the same costs 4% and 5 CTAs (48 registers)
+  // costs 4%; the fused / wide kernels spill and lose 2-10% at either
+  static constexpr int MINB1 = LOGM == 6 ? BN_CLASSICAL_2K_MINB : MINB;
   static_assert(Q >= 2 && (Q % 4) == 0, "Q must be a multiple of 4 (>= 2 for the L/H layout)");
   static_assert(G >= 1, "size too small for Q");
 };
@@ -373,7 +380,7 @@ BN_DEV void resolve_lh(const uint32_t* As, const MulCRoles<C>& ro, bool valid, u
 // five extra IMAD.MOVs on the saturated FMA-heavy pipe, 4-5% slower
 // (A/B on one B200, scripts/ab.sh).
 template <int LOGM, int Q>
-__global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
+__global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB1)
     mul_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
   using C = MulCCfg<LOGM, Q>;
   constexpr int M = C::M;
