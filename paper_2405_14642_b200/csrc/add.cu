@@ -28,6 +28,21 @@ namespace cg = cooperative_groups;
 //   0: 1024-thread clusters of 2 / 4 CTAs, 8 limbs, cp.async staging, 1 CTA/SM: 0.402 / 0.490
 //   1: one CTA x 16 limbs (512K); 2-CTA cluster x 16 limbs, direct loads (1M): 0.331 / 0.379
 //   2: clusters of 2 / 4 CTAs, 8 limbs, direct loads, 32 registers, 2 CTAs/SM: 0.310 / 0.336
+#ifndef BN_ADD6_BMIN_MID
+#define BN_ADD6_BMIN_MID 128  // 6-Add CTA size floor from 32K bits
+#endif
+#ifndef BN_ADD_BIG
+#define BN_ADD_BIG 2
+#endif
+#ifndef BN_ADD6_L12
+#define BN_ADD6_L12 16
+#endif
+#ifndef BN_ADD6_L13
+#define BN_ADD6_L13 16
+#endif
+#ifndef BN_ADD6_BMIN_MID
+#define BN_ADD6_BMIN_MID 128  // 6-Add CTA size floor from 32K bits
+#endif
 #ifndef BN_ADD_BIG
 #define BN_ADD_BIG 2
 #endif
@@ -40,11 +55,11 @@ namespace cg = cooperative_groups;
 
 namespace bn {
 
-template <int LOGM, int L>
+template <int LOGM, int L, int BMIN = 256>
 struct AddCfg {
   static constexpr int M = 1 << LOGM;
   static constexpr int TPI = M / L;
-  static constexpr int BLOCK = TPI > 256 ? TPI : 256;
+  static constexpr int BLOCK = TPI > BMIN ? TPI : BMIN;
   static constexpr int IPB = BLOCK / TPI;
 };
 
@@ -82,11 +97,11 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
 // full carry scans, each one the §2 map -> scan -> map.  The two agg
 // buffers alternate so consecutive scans need no extra barrier (a scan's
 // own __syncthreads orders every thread's previous read of the other buffer).
-template <int LOGM, int L>
-__global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
+template <int LOGM, int L, int BMIN>
+__global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
     add6_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
                 const uint32_t* __restrict__ b, uint64_t n_inst) {
-  using C = AddCfg<LOGM, L>;
+  using C = AddCfg<LOGM, L, BMIN>;
   __shared__ uint32_t agg[2][C::BLOCK / 32];
   const uint32_t slot = threadIdx.x / C::TPI;
   const uint32_t lt = threadIdx.x % C::TPI;
@@ -215,27 +230,30 @@ static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const 
   return cudaGetLastError();
 }
 
-// 6-Add limbs per thread (A/B on one box, ms per paper batch): L = 8 up to
-// 8K bits (one warp per instance); 16K: L = 16 (TPI = 32, no CTA barrier:
-// 0.335 -> 0.264 ms); 32K / 64K: L = 8 (L = 16: 0.324 -> 0.386, L = 32:
-// 0.445); 128K / 256K: L = 16 (at L = 8, 40 registers x 1024 threads left
-// one CTA per SM: 128K 0.370 -> 0.342, 256K 0.555 -> 0.377 ms).  Parking a
-// and b in shared memory (32 registers) and a cp.async double-buffered
-// persistent variant both measured slower (256K 0.435 / 0.586 ms).
+// 6-Add geometry (A/B on one box, ms per paper batch).  Limbs per thread:
+// L = 8 up to 8K bits (one warp per instance); 16K: L = 16 (TPI = 32, no
+// CTA barrier: 0.335 -> 0.264 ms); 32K: L = 8 (16: 0.386, 32: 0.445);
+// 64K, 128K, 256K: L = 16 (L = 8 at 256K: 40 registers x 1024 threads left
+// one CTA per SM, 0.555 -> 0.377 ms; L = 32: 128K 0.341 -> 0.474).  CTAs
+// from 32K bits hold one instance (BLOCK = TPI >= 128 instead of >= 256):
+// 32K 0.324 -> 0.286, 64K 0.320 -> 0.296.  Parking a and b in shared memory
+// (32 registers) and a cp.async double-buffered persistent variant both
+// measured slower (256K 0.435 / 0.586 ms).
 constexpr int add6_limbs_per_thread(int logm) {
-  return logm <= 8 ? 8 : logm == 10 ? BN_ADD6_L_LOGM10 : logm == 11 ? BN_ADD6_L_LOGM11 : 16;
+  return logm <= 8 ? 8 : logm == 9 ? 16 : logm == 10 ? 8 : logm == 11 ? 16 : logm == 12 ? BN_ADD6_L12 : BN_ADD6_L13;
 }
 
 template <int LOGM>
 static cudaError_t launch_add6_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                  cudaStream_t st, int n_sm) {
   constexpr int L = add6_limbs_per_thread(LOGM);
-  using C = AddCfg<LOGM, L>;
+  constexpr int BMIN = LOGM >= 10 ? BN_ADD6_BMIN_MID : 256;
+  using C = AddCfg<LOGM, L, BMIN>;
   const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
   const uint64_t per_sm = 2048 / C::BLOCK;
   const uint64_t cap = (uint64_t)n_sm * per_sm * 8;
   const unsigned grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
-  add6_kernel<LOGM, L><<<grid, C::BLOCK, 0, st>>>(out, a, b, n_inst);
+  add6_kernel<LOGM, L, BMIN><<<grid, C::BLOCK, 0, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
 }
 
