@@ -31,6 +31,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef BN_CLASSICAL_1K_TT
+#define BN_CLASSICAL_1K_TT 128  // target CTA size at 1K bits
+#endif
 #ifndef BN_CLASSICAL_2K_MINB
 #define BN_CLASSICAL_2K_MINB 6  // residency target of the 2K-bit 1-Mul kernel
 #endif
@@ -54,10 +57,11 @@ struct MulCCfg {
   static constexpr int Q = Q_;
   static constexpr int G = M / (2 * Q);  // column-group threads per instance
   // instances interleaved across warp lanes (keeps trip counts uniform)
-  // target threads per CTA: 256 up to 2K bits (more, smaller CTAs overlap
-  // one group's barriers / epilogue with another's convolution: -9% at 1K,
-  // -4% at 2K by A/B), 512 above (256 is 10% slower at 4K)
-  static constexpr int TT = BN_CLASSICAL_TT > 0 ? BN_CLASSICAL_TT : (LOGM <= 6 ? 256 : 512);
+  // target threads per CTA: 128 at 1K bits (A/B vs 256: 1-Mul -4%, wide
+  // -8%, Poly -8%; 64 is 28% slower), 256 at 2K (more, smaller CTAs overlap
+  // one group's barriers / epilogue with another's convolution: -4% vs 512;
+  // 128 is 27% slower), 512 above (256 is 10% slower at 4K)
+  static constexpr int TT = BN_CLASSICAL_TT > 0 ? BN_CLASSICAL_TT : (LOGM == 5 ? BN_CLASSICAL_1K_TT : LOGM == 6 ? 256 : 512);
   static constexpr int I = (TT / G) >= 32 ? 32 : ((TT / G) < 1 ? 1 : TT / G);
   static constexpr int SET_T = I * G;                         // threads per instance set
   static constexpr int SETS = SET_T >= TT ? 1 : TT / SET_T;   // sets per CTA
