@@ -763,8 +763,18 @@ static cudaError_t launch_polyc_t(uint32_t* out, const uint32_t* a, const uint32
     default: return cudaErrorInvalidValue;          \
   }
 
+template <int M, bool WIDE>
+static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                  cudaStream_t st, int n_sm);
+#ifndef BN_CLASSICAL_T1
+#define BN_CLASSICAL_T1 1  // 0: 1K bits use the column-group kernel
+#endif
+
 cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                       uint64_t n_inst, cudaStream_t st, int n_sm) {
+#if BN_CLASSICAL_T1
+  if (logm == 5) return launch_mulc_t1<32, true>(out, a, b, n_inst, st, n_sm);
+#endif
   BN_LOGM_SWITCH(launch_mulw_t, out, a, b, n_inst, st, n_sm)
 }
 
@@ -894,10 +904,120 @@ static cudaError_t launch_mulc_cluster(uint32_t* out, const uint32_t* a, const u
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ one thread per instance
+// 1K bits (M = 32): the Fig. 5 partitioning at its limit Q = M / 2, where one
+// thread owns all M columns, so there is nothing to publish or resolve: the
+// thread keeps A and B in registers and walks the columns in order (product
+// scanning), carrying the 96-bit accumulator (lo, hi, top) from column k into
+// column k + 1 — the column sums of Eq. 1 with the carry
+// resolved sequentially (the ripple of PAPER.md:125-134).  M (M + 1) / 2
+// partial products per thread, no CTA barriers.  A warp's tile is read in
+// full before its product is stored, and the next tile staged meanwhile
+// holds other instances, so in-place calls (out == a or b) are safe.
+constexpr int kT1Threads = 128;
+
+// Operands reach the registers through a per-warp shared-memory tile of 32
+// instances (A | B, 8 KiB): cp.async copies tile i + 1 (coalesced 512-byte
+// runs) while the warp multiplies tile i, so the warps of an SM do not all
+// wait on HBM at once (loading straight into registers left the FMA pipe
+// 55% busy, long-scoreboard stalls 17 per issue: ncu).  16-byte chunk c of
+// row r sits at r * 8 + (c ^ (r & 7)): a quarter-warp reading chunk k of its
+// 8 rows touches 8 distinct bank quads.
+#ifndef BN_CLASSICAL_T1_MINB
+#define BN_CLASSICAL_T1_MINB 5  // A/B at 1K (ms): 4 -> 0.395, 5 -> 0.389, 6 -> 0.398
+#endif
+// WIDE: all 2M columns (the full product, bn_mul_wide_classical).
+template <int M, bool WIDE>
+__global__ void __launch_bounds__(kT1Threads, BN_CLASSICAL_T1_MINB)
+    mul_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
+  static_assert(M == 32, "row swizzle assumes 8 chunks per row");
+  constexpr int W = kT1Threads / 32, CH = M / 4;
+  __shared__ uint4 buf[W][2][32 * CH];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint4* As = buf[wid][0];
+  uint4* Bs = buf[wid][1];
+  const uint64_t n_tiles = (n_inst + 31) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * W;
+  auto stage = [&](uint64_t tile) {
+    const uint4* ga = reinterpret_cast<const uint4*>(a) + tile * 32 * CH;
+    const uint4* gb = reinterpret_cast<const uint4*>(b) + tile * 32 * CH;
+#pragma unroll
+    for (int j = 0; j < CH; j++) {
+      const int idx = lane + 32 * j, r = idx / CH, c = idx % CH;
+      const bool valid = tile * 32 + r < n_inst;
+      cp_async16(As + r * CH + (c ^ (r & 7)), ga + idx, valid);
+      cp_async16(Bs + r * CH + (c ^ (r & 7)), gb + idx, valid);
+    }
+    cp_async_commit();
+  };
+  uint64_t tile = (uint64_t)blockIdx.x * W + wid;
+  if (tile < n_tiles) stage(tile);
+  for (; tile < n_tiles; tile += nw) {
+    uint32_t x[M], y[M];
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < CH; v++) {
+      const uint4 u = As[lane * CH + (v ^ (lane & 7))], w = Bs[lane * CH + (v ^ (lane & 7))];
+      x[4 * v] = u.x; x[4 * v + 1] = u.y; x[4 * v + 2] = u.z; x[4 * v + 3] = u.w;
+      y[4 * v] = w.x; y[4 * v + 1] = w.y; y[4 * v + 2] = w.z; y[4 * v + 3] = w.w;
+    }
+    __syncwarp();  // every lane has its row before the next tile overwrites it
+    if (tile + nw < n_tiles) stage(tile + nw);
+    constexpr int MO = WIDE ? 2 * M : M;  // output limbs
+    const uint64_t inst = tile * 32 + lane;
+    uint4* o4 = reinterpret_cast<uint4*>(out + inst * MO);
+    const bool valid = inst < n_inst;
+    uint32_t lo = 0, hi = 0, top = 0, r[4];
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+#pragma unroll
+      for (int i = 0; i <= k; i++) mac3(lo, hi, top, x[i], y[k - i]);
+      r[k & 3] = lo;
+      lo = hi;
+      hi = top;
+      top = 0;
+      if ((k & 3) == 3 && valid) o4[k / 4] = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+    if constexpr (WIDE) {
+#pragma unroll
+      for (int k = M; k < 2 * M; k++) {
+#pragma unroll
+        for (int i = k - M + 1; i < M; i++) mac3(lo, hi, top, x[i], y[k - i]);
+        r[k & 3] = lo;
+        lo = hi;
+        hi = top;
+        top = 0;
+        if ((k & 3) == 3 && valid) o4[k / 4] = make_uint4(r[0], r[1], r[2], r[3]);
+      }
+    }
+  }
+}
+
+template <int M, bool WIDE>
+static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                  cudaStream_t st, int n_sm) {
+  static LaunchCache cache;
+  int per_sm = 0;
+  cudaError_t e = resident_ctas(cache, mul_classical_t1_kernel<M, WIDE>, kT1Threads, 0, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  // persistent: one wave of CTAs, each warp walks its tiles
+  const uint64_t need = (n_inst + kT1Threads - 1) / kT1Threads;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;
+  const unsigned grid = cap_grid((unsigned)(need < cap ? need : cap));
+  mul_classical_t1_kernel<M, WIDE><<<grid, kT1Threads, 0, st>>>(out, a, b, n_inst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                  uint64_t n_inst, cudaStream_t st, int n_sm) {
   switch (logm) {
+#if BN_CLASSICAL_T1
+    case 5: return launch_mulc_t1<32, false>(out, a, b, n_inst, st, n_sm);
+#else
     case 5: return launch_mulc_t<5>(out, a, b, n_inst, st, n_sm);
+#endif
     case 6: return launch_mulc_t<6>(out, a, b, n_inst, st, n_sm);
     case 7: return launch_mulc_t<7>(out, a, b, n_inst, st, n_sm);
     case 8: return launch_mulc_t<8>(out, a, b, n_inst, st, n_sm);

@@ -50,6 +50,12 @@ constexpr int kPolyNttTT = 256;
 #ifndef BN_NTT_R32_MIN
 #define BN_NTT_R32_MIN 13
 #endif
+// r32 kernel: prefetch the next prime's / instance's raw limbs during the
+// inverse for LOGN <= this (A/B on B200, ms per paper batch: 128K 6.27 ->
+// 6.17; 256K 6.53 -> 6.66, where the 32 extra live registers add spills)
+#ifndef BN_NTT_R32_PREFETCH_MAXLOG
+#define BN_NTT_R32_PREFETCH_MAXLOG 13
+#endif
 #ifndef BN_NTT_CL_MINB
 #define BN_NTT_CL_MINB 2
 #endif
@@ -650,20 +656,35 @@ __global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
   uint32_t* Res = sm + 2 * N;    // 3 M residues
   uint32_t* agg = Res + 3 * M;   // T / 32
   const int t = threadIdx.x;
+  // Raw limbs of the next (prime, instance) step, in pass-0 layout (index
+  // t + e N/32).  With one 512-thread CTA per SM nothing else hides a load,
+  // so the limbs for prime j + 1 (or the next instance's prime 0) are issued
+  // before prime j's inverse transform and consumed after it.
+  constexpr bool PF = LOGN <= BN_NTT_R32_PREFETCH_MAXLOG;
+  uint32_t ra[16], rb[16];
+  auto fetch = [&](uint64_t i) {
+    const uint32_t* ai = a + i * M + t;
+    const uint32_t* bi = b + i * M + t;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      ra[e] = __ldg(ai + e * (N / 32));
+      rb[e] = __ldg(bi + e * (N / 32));
+    }
+  };
+  if (PF && blockIdx.x < n_inst) fetch(blockIdx.x);
   for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x) {
-    const uint32_t* ai = a + inst * M;
-    const uint32_t* bi = b + inst * M;
 #pragma unroll 1
     for (int j = 0; j < kNumPrimes; j++) {
       const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
       const uint2* twf = tw + (2 * j + 0) * (N - 1);
       const uint2* twi = tw + (2 * j + 1) * (N - 1);
       uint32_t xab[2][32];
+      if constexpr (!PF) fetch(inst);
       // N-1: limbs mod p in pass-0 layout (index t + e N/32), top half zero
 #pragma unroll
       for (int e = 0; e < 16; e++) {
-        xab[0][e] = red2(red2(__ldg(ai + t + e * (N / 32)), p2), p2);
-        xab[1][e] = red2(red2(__ldg(bi + t + e * (N / 32)), p2), p2);
+        xab[0][e] = red2(red2(ra[e], p2), p2);
+        xab[1][e] = red2(red2(rb[e], p2), p2);
       }
 #pragma unroll
       for (int e = 16; e < 32; e++) xab[0][e] = xab[1][e] = 0u;
@@ -677,6 +698,10 @@ __global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
       uint32_t x[1][32];
 #pragma unroll
       for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
+      if constexpr (PF) {
+        const uint64_t nxt = j + 1 < kNumPrimes ? inst : inst + gridDim.x;
+        if (nxt < n_inst) fetch(nxt);
+      }
       // N-4: inverse DIT, 3 passes back to the pass-0 layout
       inv_pass<LOGN, 2, 32>(x[0], t, twi, p, p2);
       xchg32<L2, L1, 1, N>(x, X, t);

@@ -73,7 +73,7 @@ def test_single_instance_and_seeds(bits):
         assert np.array_equal(inputs.to_numpy_u32(bn.mul_ntt(da, db)), w)
 
 
-@pytest.mark.parametrize("bits", [2048, 65536])
+@pytest.mark.parametrize("bits", [1024, 2048, 65536])
 def test_u64_limbs_and_in_place(bits):
     m = bits // 32
     a, b = inputs.make_operands(9, m, seed=3, cls="MIX")
@@ -90,6 +90,10 @@ def test_u64_limbs_and_in_place(bits):
         y = db.clone()
         f(da, y, out=y)  # out == b
         assert np.array_equal(inputs.to_numpy_u32(y), want), name + " in-place b"
+        z = da.clone()
+        f(z, z, out=z)  # out == a == b
+        want_sq = O.add(an, an) if name == "add" else O.mul(an, an)
+        assert np.array_equal(inputs.to_numpy_u32(z), want_sq), name + " in-place a == b"
 
 
 def test_empty_batch_and_streams():
