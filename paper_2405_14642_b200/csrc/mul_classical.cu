@@ -783,9 +783,25 @@ cudaError_t poly_classical_geometry(int logm, uint64_t n_inst, int n_sm, uint64_
   BN_LOGM_SWITCH(poly_geom_t, n_inst, n_sm, &grid, ws_words)
 }
 
+template <int M>
+static cudaError_t launch_polyc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                   cudaStream_t st, int n_sm);
+
 cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                   uint64_t n_inst, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
                                   int n_sm) {
+#if BN_CLASSICAL_T1
+  if (logm == 5) {
+    // the one-thread kernel keeps its intermediates in shared memory; the
+    // workspace contract (size check) is kept identical for every size
+    unsigned grid = 0;
+    uint64_t need = 0;
+    cudaError_t e = poly_geom_t<5>(n_inst, n_sm, &grid, &need);
+    if (e != cudaSuccess) return e;
+    if (ws_words < need) return cudaErrorInvalidValue;
+    return launch_polyc_t1<32>(out, a, b, n_inst, st, n_sm);
+  }
+#endif
   BN_LOGM_SWITCH(launch_polyc_t, out, a, b, n_inst, ws, ws_words, st, n_sm)
 }
 
@@ -1007,6 +1023,151 @@ static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32
   const uint64_t cap = (uint64_t)n_sm * per_sm;
   const unsigned grid = cap_grid((unsigned)(need < cap ? need : cap));
   mul_classical_t1_kernel<M, WIDE><<<grid, kT1Threads, 0, st>>>(out, a, b, n_inst);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ Poly, one thread per instance
+// (a a + b)(b b + b) + a b mod 2^1024 on the 1K-bit
+// one-thread-per-instance layout: four product scans, each addition folded
+// into the column accumulator of the product that precedes it (column k of
+// a a + b adds b_k before its low word is taken — the block-level fusion of
+// P:988-991 at register level).  a a and b b are squaring scans: the
+// off-diagonal column sum is formed once and doubled (272 instead of 528
+// partial products).  a b and a a + b go to this warp's shared rows, b b + b
+// stays in registers, then (a a + b)(b b + b) + a b streams to HBM.
+constexpr int kPolyT1Threads = 64;  // 2 warps x 16 KiB of shared rows per CTA
+
+BN_DEV void acc_add3(uint32_t& lo, uint32_t& hi, uint32_t& top, uint32_t c0, uint32_t c1, uint32_t c2) {
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+      : "+r"(lo), "+r"(hi), "+r"(top)
+      : "r"(c0), "r"(c1), "r"(c2));
+}
+
+// Column k of x * y (SQ: x * x, y ignored) into the running accumulator.
+template <int M, bool SQ>
+BN_DEV void t1_column(const uint32_t (&x)[M], const uint32_t (&y)[M], int k, uint32_t& lo, uint32_t& hi,
+                      uint32_t& top) {
+  if constexpr (!SQ) {
+#pragma unroll
+    for (int i = 0; i <= k; i++) mac3(lo, hi, top, x[i], y[k - i]);
+  } else {
+    uint32_t s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+    for (int i = 0; 2 * i < k; i++) mac3(s0, s1, s2, x[i], x[k - i]);
+    s2 = __funnelshift_l(s1, s2, 1);
+    s1 = __funnelshift_l(s0, s1, 1);
+    s0 <<= 1;
+    if (k % 2 == 0) mac3(s0, s1, s2, x[k / 2], x[k / 2]);
+    acc_add3(lo, hi, top, s0, s1, s2);
+  }
+}
+
+// row helpers: 16-byte chunk c of row r at r * CH + (c ^ (r & 7))
+template <int CH>
+BN_DEV void row_store4(uint4* rows, int r, int c, const uint32_t (&v)[4]) {
+  rows[r * CH + (c ^ (r & 7))] = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kPolyT1Threads)
+    poly_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
+  static_assert(M == 32, "row swizzle assumes 8 chunks per row");
+  constexpr int W = kPolyT1Threads / 32, CH = M / 4;
+  __shared__ uint4 buf[W][4][32 * CH];  // A tile | B tile | a b | a a + b
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint4* As = buf[wid][0];
+  uint4* Bs = buf[wid][1];
+  uint4* T3 = buf[wid][2];
+  uint4* T1 = buf[wid][3];
+  const uint64_t n_tiles = (n_inst + 31) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * W;
+  auto stage = [&](uint64_t tile) {
+    const uint4* ga = reinterpret_cast<const uint4*>(a) + tile * 32 * CH;
+    const uint4* gb = reinterpret_cast<const uint4*>(b) + tile * 32 * CH;
+#pragma unroll
+    for (int j = 0; j < CH; j++) {
+      const int idx = lane + 32 * j, r = idx / CH, c = idx % CH;
+      const bool valid = tile * 32 + r < n_inst;
+      cp_async16(As + r * CH + (c ^ (r & 7)), ga + idx, valid);
+      cp_async16(Bs + r * CH + (c ^ (r & 7)), gb + idx, valid);
+    }
+    cp_async_commit();
+  };
+  auto load_row = [&](const uint4* rows, uint32_t(&v)[M]) {
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+      const uint4 u = rows[lane * CH + (c ^ (lane & 7))];
+      v[4 * c] = u.x; v[4 * c + 1] = u.y; v[4 * c + 2] = u.z; v[4 * c + 3] = u.w;
+    }
+  };
+  uint64_t tile = (uint64_t)blockIdx.x * W + wid;
+  if (tile < n_tiles) stage(tile);
+  for (; tile < n_tiles; tile += nw) {
+    uint32_t x[M], y[M];
+    cp_async_wait<0>();
+    __syncwarp();
+    load_row(As, x);
+    load_row(Bs, y);
+    __syncwarp();
+    if (tile + nw < n_tiles) stage(tile + nw);
+    const uint64_t inst = tile * 32 + lane;
+    const bool valid = inst < n_inst;
+    uint32_t lo, hi, top, r[4];
+    // t3 = a b -> T3
+    lo = hi = top = 0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      t1_column<M, false>(x, y, k, lo, hi, top);
+      r[k & 3] = lo; lo = hi; hi = top; top = 0;
+      if ((k & 3) == 3) row_store4<CH>(T3, lane, k / 4, r);
+    }
+    // t1 = a a + b -> T1
+    lo = hi = top = 0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      t1_column<M, true>(x, x, k, lo, hi, top);
+      acc_add3(lo, hi, top, y[k], 0u, 0u);
+      r[k & 3] = lo; lo = hi; hi = top; top = 0;
+      if ((k & 3) == 3) row_store4<CH>(T1, lane, k / 4, r);
+    }
+    // t2 = b b + b -> registers (x is free: it takes t2)
+    lo = hi = top = 0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      t1_column<M, true>(y, y, k, lo, hi, top);
+      acc_add3(lo, hi, top, y[k], 0u, 0u);
+      x[k] = lo; lo = hi; hi = top; top = 0;
+    }
+    // out = t1 t2 + t3 (own rows only: no barrier needed)
+    load_row(T1, y);
+    uint4* o4 = reinterpret_cast<uint4*>(out + inst * M);
+    lo = hi = top = 0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      if ((k & 3) == 0) {
+        const uint4 u = T3[lane * CH + ((k / 4) ^ (lane & 7))];
+        r[0] = u.x; r[1] = u.y; r[2] = u.z; r[3] = u.w;
+      }
+      t1_column<M, false>(y, x, k, lo, hi, top);
+      acc_add3(lo, hi, top, r[k & 3], 0u, 0u);
+      r[k & 3] = lo; lo = hi; hi = top; top = 0;
+      if ((k & 3) == 3 && valid) o4[k / 4] = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+  }
+}
+
+template <int M>
+static cudaError_t launch_polyc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                   cudaStream_t st, int n_sm) {
+  static LaunchCache cache;
+  int per_sm = 0;
+  cudaError_t e = resident_ctas(cache, poly_classical_t1_kernel<M>, kPolyT1Threads, 0, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t need = (n_inst + kPolyT1Threads - 1) / kPolyT1Threads;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;
+  const unsigned grid = cap_grid((unsigned)(need < cap ? need : cap));
+  poly_classical_t1_kernel<M><<<grid, kPolyT1Threads, 0, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
 }
 

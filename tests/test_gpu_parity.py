@@ -297,8 +297,8 @@ def test_fused_grid_cap_and_workspace_reuse(bits, cap):
         assert bad is None, "%s cap=%d: %s" % (k, cap, bad)
 
 
-def test_fused_u64_in_place_and_workspace_errors():
-    m = 64
+@pytest.mark.parametrize("m", [32, 64])
+def test_fused_u64_in_place_and_workspace_errors(m):
     a, b = inputs.make_operands(33, m, seed=12, cls="U")
     an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
     da, db = a.to(DEV), b.to(DEV)
