@@ -775,6 +775,7 @@ cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a
 #if BN_CLASSICAL_T1
   if (logm == 5) return launch_mulc_t1<32, true>(out, a, b, n_inst, st, n_sm);
 #endif
+
   BN_LOGM_SWITCH(launch_mulw_t, out, a, b, n_inst, st, n_sm)
 }
 
@@ -921,7 +922,7 @@ static cudaError_t launch_mulc_cluster(uint32_t* out, const uint32_t* a, const u
 }
 
 // ------------------------------------------------------------ one thread per instance
-// 1K bits (M = 32): the Fig. 5 partitioning at its limit Q = M / 2, where one
+// 1K and 2K bits (M = 32, 64): the Fig. 5 partitioning at its limit Q = M / 2, where one
 // thread owns all M columns, so there is nothing to publish or resolve: the
 // thread keeps A and B in registers and walks the columns in order (product
 // scanning), carrying the 96-bit accumulator (lo, hi, top) from column k into
@@ -931,6 +932,8 @@ static cudaError_t launch_mulc_cluster(uint32_t* out, const uint32_t* a, const u
 // full before its product is stored, and the next tile staged meanwhile
 // holds other instances, so in-place calls (out == a or b) are safe.
 constexpr int kT1Threads = 128;
+// threads per CTA: 4 warps at 1K (8 KiB tile each), 2 at 2K (16 KiB each)
+constexpr int t1_threads(int m) { return m == 32 ? kT1Threads : 64; }
 
 // Operands reach the registers through a per-warp shared-memory tile of 32
 // instances (A | B, 8 KiB): cp.async copies tile i + 1 (coalesced 512-byte
@@ -942,12 +945,18 @@ constexpr int kT1Threads = 128;
 #ifndef BN_CLASSICAL_T1_MINB
 #define BN_CLASSICAL_T1_MINB 5  // A/B at 1K (ms): 4 -> 0.395, 5 -> 0.389, 6 -> 0.398
 #endif
+#ifndef BN_CLASSICAL_T1_MINB_2K
+#define BN_CLASSICAL_T1_MINB_2K 6  // A/B at 2K (ms): 4 -> 0.612, 6 -> 0.607 (168 registers)
+#endif
+#ifndef BN_CLASSICAL_T1_2K
+#define BN_CLASSICAL_T1_2K 1  // 2K bits one thread per instance: 0.746 -> 0.607 ms by A/B
+#endif
 // WIDE: all 2M columns (the full product, bn_mul_wide_classical).
 template <int M, bool WIDE>
-__global__ void __launch_bounds__(kT1Threads, BN_CLASSICAL_T1_MINB)
+__global__ void __launch_bounds__(t1_threads(M), M == 32 ? BN_CLASSICAL_T1_MINB : BN_CLASSICAL_T1_MINB_2K)
     mul_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
-  static_assert(M == 32, "row swizzle assumes 8 chunks per row");
-  constexpr int W = kT1Threads / 32, CH = M / 4;
+  static_assert(M % 32 == 0, "row swizzle assumes a multiple of 8 chunks per row");
+  constexpr int W = t1_threads(M) / 32, CH = M / 4;
   __shared__ uint4 buf[W][2][32 * CH];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint4* As = buf[wid][0];
@@ -1015,14 +1024,14 @@ static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32
                                   cudaStream_t st, int n_sm) {
   static LaunchCache cache;
   int per_sm = 0;
-  cudaError_t e = resident_ctas(cache, mul_classical_t1_kernel<M, WIDE>, kT1Threads, 0, &per_sm);
+  cudaError_t e = resident_ctas(cache, mul_classical_t1_kernel<M, WIDE>, t1_threads(M), 0, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   // persistent: one wave of CTAs, each warp walks its tiles
-  const uint64_t need = (n_inst + kT1Threads - 1) / kT1Threads;
+  const uint64_t need = (n_inst + t1_threads(M) - 1) / t1_threads(M);
   const uint64_t cap = (uint64_t)n_sm * per_sm;
   const unsigned grid = cap_grid((unsigned)(need < cap ? need : cap));
-  mul_classical_t1_kernel<M, WIDE><<<grid, kT1Threads, 0, st>>>(out, a, b, n_inst);
+  mul_classical_t1_kernel<M, WIDE><<<grid, t1_threads(M), 0, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
 }
 
@@ -1179,7 +1188,11 @@ cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, con
 #else
     case 5: return launch_mulc_t<5>(out, a, b, n_inst, st, n_sm);
 #endif
+#if BN_CLASSICAL_T1_2K
+    case 6: return launch_mulc_t1<64, false>(out, a, b, n_inst, st, n_sm);
+#else
     case 6: return launch_mulc_t<6>(out, a, b, n_inst, st, n_sm);
+#endif
     case 7: return launch_mulc_t<7>(out, a, b, n_inst, st, n_sm);
     case 8: return launch_mulc_t<8>(out, a, b, n_inst, st, n_sm);
     case 9: return launch_mulc_t<9>(out, a, b, n_inst, st, n_sm);
