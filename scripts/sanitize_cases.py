@@ -15,7 +15,7 @@ from paper_2405_14642_b200 import bn, inputs  # noqa: E402
 dev = torch.device("cuda:0")
 bn.prepare(0)
 bad = 0
-cases = [(1024, 37), (4096, 19), (65536, 3), (262144, 1)]
+cases = [(1024, 37), (2048, 41), (4096, 19), (65536, 3), (131072, 2), (262144, 1)]
 if "--big" in sys.argv:
     cases += [(1 << 19, 2), (1 << 20, 1)]
 for cap in (0, 2):
