@@ -769,11 +769,17 @@ static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32
 #ifndef BN_CLASSICAL_T1
 #define BN_CLASSICAL_T1 1  // 0: 1K bits use the column-group kernel
 #endif
+#ifndef BN_CLASSICAL_T1_WIDE_2K
+#define BN_CLASSICAL_T1_WIDE_2K 1  // wide 2K one thread per instance: 1.754 -> 1.240 ms by A/B
+#endif
 
 cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                       uint64_t n_inst, cudaStream_t st, int n_sm) {
 #if BN_CLASSICAL_T1
   if (logm == 5) return launch_mulc_t1<32, true>(out, a, b, n_inst, st, n_sm);
+#endif
+#if BN_CLASSICAL_T1_WIDE_2K
+  if (logm == 6) return launch_mulc_t1<64, true>(out, a, b, n_inst, st, n_sm);
 #endif
 
   BN_LOGM_SWITCH(launch_mulw_t, out, a, b, n_inst, st, n_sm)
@@ -1005,8 +1011,20 @@ __global__ void __launch_bounds__(t1_threads(M), M == 32 ? BN_CLASSICAL_T1_MINB 
       if ((k & 3) == 3 && valid) o4[k / 4] = make_uint4(r[0], r[1], r[2], r[3]);
     }
     if constexpr (WIDE) {
+      // upper columns in two loop nests (one nest of M columns does not
+      // unroll at M = 64, and the operand arrays would go to the stack)
 #pragma unroll
-      for (int k = M; k < 2 * M; k++) {
+      for (int k = M; k < 3 * M / 2; k++) {
+#pragma unroll
+        for (int i = k - M + 1; i < M; i++) mac3(lo, hi, top, x[i], y[k - i]);
+        r[k & 3] = lo;
+        lo = hi;
+        hi = top;
+        top = 0;
+        if ((k & 3) == 3 && valid) o4[k / 4] = make_uint4(r[0], r[1], r[2], r[3]);
+      }
+#pragma unroll
+      for (int k = 3 * M / 2; k < 2 * M; k++) {
 #pragma unroll
         for (int i = k - M + 1; i < M; i++) mac3(lo, hi, top, x[i], y[k - i]);
         r[k & 3] = lo;
