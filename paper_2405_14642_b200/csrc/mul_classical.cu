@@ -793,20 +793,23 @@ cudaError_t poly_classical_geometry(int logm, uint64_t n_inst, int n_sm, uint64_
 template <int M>
 static cudaError_t launch_polyc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                    cudaStream_t st, int n_sm);
+#ifndef BN_POLY_T1_2K
+#define BN_POLY_T1_2K 1
+#endif
 
 cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                   uint64_t n_inst, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
                                   int n_sm) {
 #if BN_CLASSICAL_T1
-  if (logm == 5) {
+  if (logm == 5 || (BN_POLY_T1_2K && logm == 6)) {
     // the one-thread kernel keeps its intermediates in shared memory; the
     // workspace contract (size check) is kept identical for every size
     unsigned grid = 0;
     uint64_t need = 0;
-    cudaError_t e = poly_geom_t<5>(n_inst, n_sm, &grid, &need);
+    cudaError_t e = logm == 5 ? poly_geom_t<5>(n_inst, n_sm, &grid, &need) : poly_geom_t<6>(n_inst, n_sm, &grid, &need);
     if (e != cudaSuccess) return e;
     if (ws_words < need) return cudaErrorInvalidValue;
-    return launch_polyc_t1<32>(out, a, b, n_inst, st, n_sm);
+    return logm == 5 ? launch_polyc_t1<32>(out, a, b, n_inst, st, n_sm) : launch_polyc_t1<64>(out, a, b, n_inst, st, n_sm);
   }
 #endif
   BN_LOGM_SWITCH(launch_polyc_t, out, a, b, n_inst, ws, ws_words, st, n_sm)
@@ -1095,17 +1098,52 @@ BN_DEV void row_store4(uint4* rows, int r, int c, const uint32_t (&v)[4]) {
   rows[r * CH + (c ^ (r & 7))] = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
+// Columns [K0, K1) of x * y (SQ: x * x): add(k, lo, hi, top) folds an addend
+// into column k, sink(k, lo) takes its low word.
+template <int M, bool SQ, int K0, int K1, class Add, class Sink>
+BN_DEV void t1_cols(const uint32_t (&x)[M], const uint32_t (&y)[M], uint32_t& lo, uint32_t& hi, uint32_t& top,
+                    Add add, Sink sink) {
+#pragma unroll
+  for (int k = K0; k < K1; k++) {
+    t1_column<M, SQ>(x, y, k, lo, hi, top);
+    add(k, lo, hi, top);
+    sink(k, lo);
+    lo = hi;
+    hi = top;
+    top = 0;
+  }
+}
+// the M columns of one truncated product; at M = 64 as two loop nests (one
+// nest does not unroll and the operand arrays would go to the stack)
+template <int M, bool SQ, class Add, class Sink>
+BN_DEV void t1_prod(const uint32_t (&x)[M], const uint32_t (&y)[M], Add add, Sink sink) {
+  uint32_t lo = 0, hi = 0, top = 0;
+  if constexpr (M <= 32) {
+    t1_cols<M, SQ, 0, M>(x, y, lo, hi, top, add, sink);
+  } else {
+    t1_cols<M, SQ, 0, M / 2>(x, y, lo, hi, top, add, sink);
+    t1_cols<M, SQ, M / 2, M>(x, y, lo, hi, top, add, sink);
+  }
+}
+
+// 2K (M = 64): the operand tile alone is 16 KiB per warp, so a b and a a + b
+// overwrite it (each lane its own rows) and the next tile is loaded after
+// the product instead of during it (PF = false).
+#ifndef BN_POLY_T1_MINB
+#define BN_POLY_T1_MINB 6  // 168 registers, 6 CTAs x 32 KiB per SM
+#endif
 template <int M>
-__global__ void __launch_bounds__(kPolyT1Threads)
+__global__ void __launch_bounds__(kPolyT1Threads, BN_POLY_T1_MINB)
     poly_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
-  static_assert(M == 32, "row swizzle assumes 8 chunks per row");
-  constexpr int W = kPolyT1Threads / 32, CH = M / 4;
-  __shared__ uint4 buf[W][4][32 * CH];  // A tile | B tile | a b | a a + b
+  static_assert(M % 32 == 0, "row swizzle assumes a multiple of 8 chunks per row");
+  constexpr bool PF = M == 32;
+  constexpr int W = kPolyT1Threads / 32, CH = M / 4, NB = PF ? 4 : 2;
+  __shared__ uint4 buf[W][NB][32 * CH];  // A tile | B tile [| a b | a a + b]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint4* As = buf[wid][0];
   uint4* Bs = buf[wid][1];
-  uint4* T3 = buf[wid][2];
-  uint4* T1 = buf[wid][3];
+  uint4* T3 = buf[wid][PF ? 2 : 0];
+  uint4* T1 = buf[wid][PF ? 3 : 1];
   const uint64_t n_tiles = (n_inst + 31) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * W;
   auto stage = [&](uint64_t tile) {
@@ -1128,58 +1166,49 @@ __global__ void __launch_bounds__(kPolyT1Threads)
     }
   };
   uint64_t tile = (uint64_t)blockIdx.x * W + wid;
-  if (tile < n_tiles) stage(tile);
+  if (PF && tile < n_tiles) stage(tile);
   for (; tile < n_tiles; tile += nw) {
     uint32_t x[M], y[M];
+    if constexpr (!PF) {
+      __syncwarp();  // every lane is done with its rows of the previous tile
+      stage(tile);
+    }
     cp_async_wait<0>();
     __syncwarp();
     load_row(As, x);
     load_row(Bs, y);
     __syncwarp();
-    if (tile + nw < n_tiles) stage(tile + nw);
+    if (PF && tile + nw < n_tiles) stage(tile + nw);
     const uint64_t inst = tile * 32 + lane;
     const bool valid = inst < n_inst;
-    uint32_t lo, hi, top, r[4];
+    uint32_t r[4];
+    auto none = [](int, uint32_t&, uint32_t&, uint32_t&) {};
+    auto plus_b = [&](int k, uint32_t& lo, uint32_t& hi, uint32_t& top) { acc_add3(lo, hi, top, y[k], 0u, 0u); };
     // t3 = a b -> T3
-    lo = hi = top = 0;
-#pragma unroll
-    for (int k = 0; k < M; k++) {
-      t1_column<M, false>(x, y, k, lo, hi, top);
-      r[k & 3] = lo; lo = hi; hi = top; top = 0;
+    t1_prod<M, false>(x, y, none, [&](int k, uint32_t lo) {
+      r[k & 3] = lo;
       if ((k & 3) == 3) row_store4<CH>(T3, lane, k / 4, r);
-    }
+    });
     // t1 = a a + b -> T1
-    lo = hi = top = 0;
-#pragma unroll
-    for (int k = 0; k < M; k++) {
-      t1_column<M, true>(x, x, k, lo, hi, top);
-      acc_add3(lo, hi, top, y[k], 0u, 0u);
-      r[k & 3] = lo; lo = hi; hi = top; top = 0;
+    t1_prod<M, true>(x, x, plus_b, [&](int k, uint32_t lo) {
+      r[k & 3] = lo;
       if ((k & 3) == 3) row_store4<CH>(T1, lane, k / 4, r);
-    }
+    });
     // t2 = b b + b -> registers (x is free: it takes t2)
-    lo = hi = top = 0;
-#pragma unroll
-    for (int k = 0; k < M; k++) {
-      t1_column<M, true>(y, y, k, lo, hi, top);
-      acc_add3(lo, hi, top, y[k], 0u, 0u);
-      x[k] = lo; lo = hi; hi = top; top = 0;
-    }
+    t1_prod<M, true>(y, y, plus_b, [&](int k, uint32_t lo) { x[k] = lo; });
     // out = t1 t2 + t3 (own rows only: no barrier needed)
     load_row(T1, y);
     uint4* o4 = reinterpret_cast<uint4*>(out + inst * M);
-    lo = hi = top = 0;
-#pragma unroll
-    for (int k = 0; k < M; k++) {
+    t1_prod<M, false>(y, x, [&](int k, uint32_t& lo, uint32_t& hi, uint32_t& top) {
       if ((k & 3) == 0) {
         const uint4 u = T3[lane * CH + ((k / 4) ^ (lane & 7))];
         r[0] = u.x; r[1] = u.y; r[2] = u.z; r[3] = u.w;
       }
-      t1_column<M, false>(y, x, k, lo, hi, top);
       acc_add3(lo, hi, top, r[k & 3], 0u, 0u);
-      r[k & 3] = lo; lo = hi; hi = top; top = 0;
+    }, [&](int k, uint32_t lo) {
+      r[k & 3] = lo;
       if ((k & 3) == 3 && valid) o4[k / 4] = make_uint4(r[0], r[1], r[2], r[3]);
-    }
+    });
   }
 }
 
