@@ -46,6 +46,12 @@ namespace cg = cooperative_groups;
 #endif
 // the Poly kernel keeps 256-thread CTAs (64 measured 26% slower for it)
 constexpr int kPolyNttTT = 256;
+// residency target (threads per SM) of the 16-element kernel for N <= 256.
+// A/B at 4K (ms): 768 -> 2.882 (80 registers), 896 -> 2.891 (72), 1024 ->
+// 2.921 (64; shared memory caps all three at 12-14 CTAs of 64 threads)
+#ifndef BN_NTT_SMALL_THREADS
+#define BN_NTT_SMALL_THREADS 768
+#endif
 // smallest log2 N that uses the 32-element-per-thread kernel
 #ifndef BN_NTT_R32_MIN
 #define BN_NTT_R32_MIN 13
@@ -123,7 +129,7 @@ struct NttCfg {
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
   // (A/B on B200: best of {3,4} x {2,3} for T = 256; 2 for T = 512; T = 1024
   // must keep 64 registers)
-  static constexpr int MINB = LOGN <= 8 ? (768 / T > 1 ? 768 / T : 1)
+  static constexpr int MINB = LOGN <= 8 ? (BN_NTT_SMALL_THREADS / T > 1 ? BN_NTT_SMALL_THREADS / T : 1)
                                         : (T <= 256 ? (512 / T > 1 ? 512 / T : 1) : (T == 512 ? 2 : 1));
 };
 
