@@ -940,9 +940,9 @@ static cudaError_t launch_mulc_cluster(uint32_t* out, const uint32_t* a, const u
 // partial products per thread, no CTA barriers.  A warp's tile is read in
 // full before its product is stored, and the next tile staged meanwhile
 // holds other instances, so in-place calls (out == a or b) are safe.
+// threads per CTA: 4 warps for the 1K 1-Mul (one 8 KiB stage each), else 2
+// (the 1K full product with two stages, 2K with one 16 KiB stage per warp)
 constexpr int kT1Threads = 128;
-// threads per CTA: 4 warps at 1K (8 KiB tile each), 2 at 2K (16 KiB each)
-constexpr int t1_threads(int m) { return m == 32 ? kT1Threads : 64; }
 
 // Operands reach the registers through a per-warp shared-memory tile of 32
 // instances (A | B, 8 KiB): cp.async copies tile i + 1 (coalesced 512-byte
@@ -960,44 +960,56 @@ constexpr int t1_threads(int m) { return m == 32 ? kT1Threads : 64; }
 #ifndef BN_CLASSICAL_T1_2K
 #define BN_CLASSICAL_T1_2K 1  // 2K bits one thread per instance: 0.746 -> 0.607 ms by A/B
 #endif
+// tiles in flight per warp (cp.async stages of A | B); A/B at 1K (ms):
+// 1-Mul 1 stage 0.348 / 2 stages 0.368, full product 0.697 / 0.635
+constexpr int t1_stages(int m, bool wide) { return m == 32 && wide ? 2 : 1; }
+constexpr int t1_threads(int m, bool wide) { return m == 32 && t1_stages(m, wide) == 1 ? kT1Threads : 64; }
+constexpr int t1_minb(int m, bool wide) { return m == 32 && !wide ? BN_CLASSICAL_T1_MINB : BN_CLASSICAL_T1_MINB_2K; }
 // WIDE: all 2M columns (the full product, bn_mul_wide_classical).
 template <int M, bool WIDE>
-__global__ void __launch_bounds__(t1_threads(M), M == 32 ? BN_CLASSICAL_T1_MINB : BN_CLASSICAL_T1_MINB_2K)
+__global__ void __launch_bounds__(t1_threads(M, WIDE), t1_minb(M, WIDE))
     mul_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
   static_assert(M % 32 == 0, "row swizzle assumes a multiple of 8 chunks per row");
-  constexpr int W = t1_threads(M) / 32, CH = M / 4;
-  __shared__ uint4 buf[W][2][32 * CH];
+  constexpr int W = t1_threads(M, WIDE) / 32, CH = M / 4, NS = t1_stages(M, WIDE);
+  __shared__ uint4 buf[W][NS][2][32 * CH];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint4* As = buf[wid][0];
-  uint4* Bs = buf[wid][1];
   const uint64_t n_tiles = (n_inst + 31) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * W;
-  auto stage = [&](uint64_t tile) {
-    const uint4* ga = reinterpret_cast<const uint4*>(a) + tile * 32 * CH;
-    const uint4* gb = reinterpret_cast<const uint4*>(b) + tile * 32 * CH;
+  // stage st holds tile number it (0, 1, ...) of this warp with it % NS == st;
+  // one commit group per tile (empty past the end) keeps the wait counts uniform
+  auto stage = [&](uint64_t tile, int st) {
+    if (tile < n_tiles) {
+      uint4* As = buf[wid][st][0];
+      uint4* Bs = buf[wid][st][1];
+      const uint4* ga = reinterpret_cast<const uint4*>(a) + tile * 32 * CH;
+      const uint4* gb = reinterpret_cast<const uint4*>(b) + tile * 32 * CH;
 #pragma unroll
-    for (int j = 0; j < CH; j++) {
-      const int idx = lane + 32 * j, r = idx / CH, c = idx % CH;
-      const bool valid = tile * 32 + r < n_inst;
-      cp_async16(As + r * CH + (c ^ (r & 7)), ga + idx, valid);
-      cp_async16(Bs + r * CH + (c ^ (r & 7)), gb + idx, valid);
+      for (int j = 0; j < CH; j++) {
+        const int idx = lane + 32 * j, r = idx / CH, c = idx % CH;
+        const bool valid = tile * 32 + r < n_inst;
+        cp_async16(As + r * CH + (c ^ (r & 7)), ga + idx, valid);
+        cp_async16(Bs + r * CH + (c ^ (r & 7)), gb + idx, valid);
+      }
     }
     cp_async_commit();
   };
   uint64_t tile = (uint64_t)blockIdx.x * W + wid;
-  if (tile < n_tiles) stage(tile);
-  for (; tile < n_tiles; tile += nw) {
+#pragma unroll
+  for (int k = 0; k < NS; k++) stage(tile + k * nw, k);
+  for (int st = 0; tile < n_tiles; tile += nw, st = st + 1 == NS ? 0 : st + 1) {
     uint32_t x[M], y[M];
-    cp_async_wait<0>();
+    cp_async_wait<NS - 1>();
     __syncwarp();
+    const uint4* As = buf[wid][st][0];
+    const uint4* Bs = buf[wid][st][1];
 #pragma unroll
     for (int v = 0; v < CH; v++) {
       const uint4 u = As[lane * CH + (v ^ (lane & 7))], w = Bs[lane * CH + (v ^ (lane & 7))];
       x[4 * v] = u.x; x[4 * v + 1] = u.y; x[4 * v + 2] = u.z; x[4 * v + 3] = u.w;
       y[4 * v] = w.x; y[4 * v + 1] = w.y; y[4 * v + 2] = w.z; y[4 * v + 3] = w.w;
     }
-    __syncwarp();  // every lane has its row before the next tile overwrites it
-    if (tile + nw < n_tiles) stage(tile + nw);
+    __syncwarp();  // every lane has its row before the stage is refilled
+    stage(tile + NS * nw, st);
     constexpr int MO = WIDE ? 2 * M : M;  // output limbs
     const uint64_t inst = tile * 32 + lane;
     uint4* o4 = reinterpret_cast<uint4*>(out + inst * MO);
@@ -1045,14 +1057,14 @@ static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32
                                   cudaStream_t st, int n_sm) {
   static LaunchCache cache;
   int per_sm = 0;
-  cudaError_t e = resident_ctas(cache, mul_classical_t1_kernel<M, WIDE>, t1_threads(M), 0, &per_sm);
+  cudaError_t e = resident_ctas(cache, mul_classical_t1_kernel<M, WIDE>, t1_threads(M, WIDE), 0, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   // persistent: one wave of CTAs, each warp walks its tiles
-  const uint64_t need = (n_inst + t1_threads(M) - 1) / t1_threads(M);
+  const uint64_t need = (n_inst + t1_threads(M, WIDE) - 1) / t1_threads(M, WIDE);
   const uint64_t cap = (uint64_t)n_sm * per_sm;
   const unsigned grid = cap_grid((unsigned)(need < cap ? need : cap));
-  mul_classical_t1_kernel<M, WIDE><<<grid, t1_threads(M), 0, st>>>(out, a, b, n_inst);
+  mul_classical_t1_kernel<M, WIDE><<<grid, t1_threads(M, WIDE), 0, st>>>(out, a, b, n_inst);
   return cudaGetLastError();
 }
 
