@@ -931,8 +931,9 @@ static cudaError_t launch_mulc_cluster(uint32_t* out, const uint32_t* a, const u
 }
 
 // ------------------------------------------------------------ one thread per instance
-// 1K and 2K bits (M = 32, 64): the Fig. 5 partitioning at its limit Q = M / 2, where one
-// thread owns all M columns, so there is nothing to publish or resolve: the
+// 1K and 2K bits (M = 32, 64): the Fig. 5 partitioning at its limit
+// Q = M / 2, where one thread owns all M columns, so there is nothing to
+// publish or resolve: the
 // thread keeps A and B in registers and walks the columns in order (product
 // scanning), carrying the 96-bit accumulator (lo, hi, top) from column k into
 // column k + 1 — the column sums of Eq. 1 with the carry
@@ -1069,7 +1070,7 @@ static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32
 }
 
 // ------------------------------------------------------------ Poly, one thread per instance
-// (a a + b)(b b + b) + a b mod 2^1024 on the 1K-bit
+// (a a + b)(b b + b) + a b mod 2^(32 M) on the 1K / 2K-bit
 // one-thread-per-instance layout: four product scans, each addition folded
 // into the column accumulator of the product that precedes it (column k of
 // a a + b adds b_k before its low word is taken — the block-level fusion of
