@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 // -DBN_NTT14_CLUSTER -DBN_NTT_CL_T=512 [-DBN_NTT_CL_MINB=1] rebuild the variants.
 // target CTA size of the 16-element kernel for N <= 256 (several instances per CTA)
 #ifndef BN_NTT_TT
-#define BN_NTT_TT 64  // A/B at 4K: 256 -> 2.953 ms, 128 -> 2.879, 64 -> 2.873
+#define BN_NTT_TT 64  // A/B at 4K: 256 -> 2.953 ms, 128 -> 2.879, 64 -> 2.873, 32 -> 2.884
 #endif
 #ifndef BN_NTT_TT_MAXLOG
 #define BN_NTT_TT_MAXLOG 12  // A/B: 16K -9.4%, 32K -7.7% vs 256-thread CTAs
