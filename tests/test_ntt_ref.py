@@ -136,6 +136,56 @@ def test_cyclic_no_padding_is_wrong():
     assert R.fft_mul_paper(A, A, n, d, f) != (A * A) % (1 << (d * n))
 
 
+def _cyclic_product_by_hand(A, B, M, d, p):
+    """The value bmulFFT must return, written without any
+    transform: digits a_i, b_j of A, B (d bits, M of them); the cyclic
+    coefficient c_k = sum over i + j == k (mod M) of a_i * b_j, reduced mod p;
+    then sum c_k 2^(d k) carried mod 2^(d M) (M-point transform
+    on M digits, no zero padding)."""
+    a = [(A >> (d * i)) & ((1 << d) - 1) for i in range(M)]
+    b = [(B >> (d * j)) & ((1 << d) - 1) for j in range(M)]
+    c = [0] * M
+    for i in range(M):
+        for j in range(M):
+            c[(i + j) % M] += a[i] * b[j]
+    return sum((ck % p) << (d * k) for k, ck in enumerate(c)) % (1 << (d * M))
+
+
+@pytest.mark.parametrize("field", ["PF32", "PF64"])
+@pytest.mark.parametrize("M", [4, 8, 16])
+def test_fft_mul_paper_is_cyclic_convolution(field, M):
+    """Pin of fft_mul_paper (bmulFFT as printed):
+    it must equal the cyclic convolution of the digit vectors mod p, carried
+    in base 2^d — computed by the double loop above, no DFT involved.  A
+    wrong inverse twiddle direction (c_k -> c_{-k}), a missing or wrong invM,
+    or a dropped wrap term all change the result on these random digits."""
+    f = R.PRIME_FIELD_32 if field == "PF32" else R.PRIME_FIELD_64
+    p = f["p"]
+    rng = random.Random(1000 * M + (32 if field == "PF32" else 64))
+    for d in (8, 15) if field == "PF32" else (16, 31):
+        for _ in range(4):
+            A, B = rng.getrandbits(d * M), rng.getrandbits(d * M)
+            assert R.fft_mul_paper(A, B, M, d, f) == _cyclic_product_by_hand(A, B, M, d, p)
+        # coefficients that exceed p (all-max digits) are reduced mod p, not kept
+        A = (1 << (d * M)) - 1
+        assert R.fft_mul_paper(A, A, M, d, f) == _cyclic_product_by_hand(A, A, M, d, p)
+
+
+@pytest.mark.parametrize("field", ["PF32", "PF64"])
+def test_fft_mul_paper_exact_when_wrap_vanishes(field):
+    """Positive case of bmulFFT: when A has a single nonzero digit (A < 2^d),
+    c_k = a_0 b_k, nothing wraps and nothing exceeds p, so the printed
+    scheme returns the true product A*B mod 2^(dM) (Eq. 1)."""
+    f = R.PRIME_FIELD_32 if field == "PF32" else R.PRIME_FIELD_64
+    rng = random.Random(7)
+    d = 12 if field == "PF32" else 24
+    for M in (4, 8, 16):
+        for _ in range(3):
+            A, B = rng.getrandbits(d), rng.getrandbits(d * M)
+            assert R.fft_mul_paper(A, B, M, d, f) == (A * B) % (1 << (d * M))
+        assert R.fft_mul_paper(1, B, M, d, f) == B
+
+
 def _find_primes(count, lo_bits=29, hi=1 << 30, two_adicity=15):
     out, k = [], (hi - 1) >> two_adicity
     while len(out) < count:
