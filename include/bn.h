@@ -31,7 +31,16 @@
  *
  * STREAMS: every call is stream-ordered and asynchronous on `stream`
  * (a cudaStream_t; NULL = legacy default stream), performs no allocation and
- * no host synchronisation (bn_prepare excepted).
+ * no host synchronisation — once the device is initialised.  The FIRST call
+ * of any entry point on a device initialises it (bn_prepare: one cudaMalloc
+ * of the NTT tables and synchronous uploads), so call bn_prepare(device)
+ * up front when the first call must be asynchronous or is made under
+ * CUDA-graph stream capture (an initialising call inside a capture fails).
+ *
+ * ALIASING AND ORDER: in-place calls are safe because every CTA reads all
+ * of an instance's limbs before any write to that instance, and only the
+ * thread that read a limb (add) or the CTA that staged the instance (mul)
+ * writes it; the kernels therefore do not declare out / a / b __restrict__.
  *
  * ERRORS: argument errors return synchronously before any launch and write
  * nothing; a failed launch returns BN_ECUDA (see bn_cuda_error()); device
@@ -56,7 +65,7 @@ typedef enum {
     BN_EALIGN = 3, /* a, b or out not 16-byte aligned */
     BN_EALIAS = 4, /* out partially overlaps a or b (exact equality allowed) */
     BN_ECUDA = 5,  /* CUDA launch / configuration / copy failure */
-    BN_ENODEV = 6  /* no usable sm_100 device */
+    BN_ENODEV = 6  /* no usable device: the library holds sm_100a code only (CC 10.0) */
 } bn_status;
 
 /*
@@ -151,8 +160,9 @@ bn_status bn_mul_wide_classical(void *out, const void *a, const void *b, uint64_
 bn_status bn_mul_wide_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
                           uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
 
-/* Build the NTT twiddle/CRT tables for `device` (all sizes), synchronously.
- * Idempotent and thread-safe; bn_mul_ntt calls it lazily. */
+/* Initialise `device`: check it is CC 10.0 (else BN_ENODEV), build the NTT
+ * twiddle/CRT tables (all sizes) and upload them, synchronously.  Idempotent
+ * and thread-safe; every other entry point calls it lazily on first use. */
 bn_status bn_prepare(int device);
 
 /* ---- host-buffer entry point (end-to-end path) ---------------------------

@@ -40,18 +40,6 @@ namespace cg = cooperative_groups;
 #ifndef BN_ADD6_L13
 #define BN_ADD6_L13 16
 #endif
-#ifndef BN_ADD6_BMIN_MID
-#define BN_ADD6_BMIN_MID 128  // 6-Add CTA size floor from 32K bits
-#endif
-#ifndef BN_ADD_BIG
-#define BN_ADD_BIG 2
-#endif
-#ifndef BN_ADD6_L_LOGM10
-#define BN_ADD6_L_LOGM10 8
-#endif
-#ifndef BN_ADD6_L_LOGM11
-#define BN_ADD6_L_LOGM11 8
-#endif
 
 namespace bn {
 
@@ -65,8 +53,8 @@ struct AddCfg {
 
 template <int LOGM, int L>
 __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
-    add_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
-               const uint32_t* __restrict__ b, uint64_t n_inst) {
+    add_kernel(uint32_t* out, const uint32_t* a,
+               const uint32_t* b, uint64_t n_inst) {
   using C = AddCfg<LOGM, L>;
   __shared__ uint32_t agg[C::BLOCK / 32];
   const uint32_t slot = threadIdx.x / C::TPI;  // instance slot in the CTA
@@ -99,8 +87,8 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L>::BLOCK)
 // own __syncthreads orders every thread's previous read of the other buffer).
 template <int LOGM, int L, int BMIN>
 __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
-    add6_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
-                const uint32_t* __restrict__ b, uint64_t n_inst) {
+    add6_kernel(uint32_t* out, const uint32_t* a,
+                const uint32_t* b, uint64_t n_inst) {
   using C = AddCfg<LOGM, L, BMIN>;
   __shared__ uint32_t agg[2][C::BLOCK / 32];
   const uint32_t slot = threadIdx.x / C::TPI;
@@ -144,8 +132,8 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
 // one's loads overlap the other's cluster barrier — the default (BN_ADD_BIG).
 template <int LOGM, int L, int NS, int MB>
 __global__ void __launch_bounds__(1024, MB)
-    add_cluster_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ a,
-                       const uint32_t* __restrict__ b, uint64_t n_inst) {
+    add_cluster_kernel(uint32_t* out, const uint32_t* a,
+                       const uint32_t* b, uint64_t n_inst) {
   constexpr int M = 1 << LOGM, CR = M / (1024 * L), SL = M / CR;  // limbs per CTA
   extern __shared__ __align__(16) uint32_t sm[];  // [NS stages][a | b][SL]
   __shared__ uint32_t agg[32];

@@ -4,6 +4,7 @@
 // mul_classical.cu and mul_ntt.cu.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -98,7 +99,8 @@ uint32_t primitive_root(uint32_t p) {
 
 // ---------------------------------------------------------------- per-device state
 struct DevState {
-  bool ready = false;
+  // set (release) once the tables are uploaded; read (acquire) without the lock
+  std::atomic<bool> ready{false};
   int n_sm = 0;
   uint2* tw_dev = nullptr;
   bn::NttTables tables[bn::kMaxLogN + 1];
@@ -203,17 +205,19 @@ bn_status build_tables(DevState& d) {
 bn_status ensure_device(int dev, DevState** out) {
   if (dev < 0 || dev >= kMaxDev) return BN_ENODEV;
   DevState& d = g_dev[dev];
-  if (d.ready) {
+  if (d.ready.load(std::memory_order_acquire)) {
     *out = &d;
     return BN_OK;
   }
   std::lock_guard<std::mutex> lk(g_mu);
-  if (!d.ready) {
+  if (!d.ready.load(std::memory_order_relaxed)) {
     if (!host_consts()) return BN_EINVAL;
     cudaDeviceProp prop;
     cudaError_t e = cudaGetDeviceProperties(&prop, dev);
     if (e != cudaSuccess) return cuda_fail(e);
-    if (prop.major < 10) return BN_ENODEV;  // sm_100a binary only
+    // the library holds sm_100a code only: any other compute capability
+    // (10.x with x != 0, 12.x, ...) cannot load it
+    if (prop.major != 10 || prop.minor != 0) return BN_ENODEV;
     d.n_sm = prop.multiProcessorCount;
     int prev = 0;
     cudaGetDevice(&prev);
@@ -221,7 +225,7 @@ bn_status ensure_device(int dev, DevState** out) {
     bn_status st = build_tables(d);
     if (prev != dev) cudaSetDevice(prev);
     if (st != BN_OK) return st;
-    d.ready = true;
+    d.ready.store(true, std::memory_order_release);
   }
   *out = &d;
   return BN_OK;
@@ -471,6 +475,17 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   }
   const char* ha = (const char*)a;
   const char* hb = (const char*)b;
+  // on any failure, drain both streams before returning: copies and kernels
+  // of earlier chunks must not keep writing into the caller's host buffers
+  // (or reading this scratch) after the call has returned
+  auto fail = [&](bn_status st) {
+    for (int i = 0; i < 2; i++) (void)cudaStreamSynchronize(d->st[i]);
+    return st;
+  };
+  auto fail_cuda = [&](cudaError_t err) {
+    const bn_status st = cuda_fail(err);
+    return fail(st);
+  };
   uint64_t c = 0;
   for (uint64_t i0 = 0; i0 < n_inst; i0 += chunk, c++) {
     const uint64_t n = (n_inst - i0) < chunk ? (n_inst - i0) : chunk;
@@ -480,9 +495,9 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
     uint32_t* da = (uint32_t*)base;
     uint32_t* db = (uint32_t*)(base + chunk_bytes);
     e = cudaMemcpyAsync(da, ha + i0 * inst_bytes, bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (e != cudaSuccess) return fail_cuda(e);
     e = cudaMemcpyAsync(db, hb + i0 * inst_bytes, bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (e != cudaSuccess) return fail_cuda(e);
     for (int k = 0; k < n_ops; k++) {
       uint32_t* dout = (uint32_t*)(base + (2 + k) * chunk_bytes);
       uint32_t* dws = (uint32_t*)(base + (2 + n_ops) * chunk_bytes);
@@ -493,18 +508,18 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
         case BN_OP_ADD6: e = bn::launch_add6(logm, dout, da, db, n, st, d->n_sm); break;
         default: {
           s = launch_poly(ops[k], logm, dout, da, db, n, dws, ws_words, st, d);
-          if (s != BN_OK) return s;
+          if (s != BN_OK) return fail(s);
           e = cudaSuccess;
         }
       }
-      if (e != cudaSuccess) return cuda_fail(e);
+      if (e != cudaSuccess) return fail_cuda(e);
       e = cudaMemcpyAsync((char*)outs[k] + i0 * inst_bytes, dout, bytes, cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) return cuda_fail(e);
+      if (e != cudaSuccess) return fail_cuda(e);
     }
   }
   for (int i = 0; i < 2; i++) {
     e = cudaStreamSynchronize(d->st[i]);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (e != cudaSuccess) return fail_cuda(e);
   }
   return BN_OK;
 }

@@ -37,3 +37,45 @@ def max_over_ranks(value: float, dist=None, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def plan(rank: int, world: int, n: int, scaling: str):
+    """This rank's global instance range [lo, hi) and the job's total.
+
+    weak:   n instances per rank (the paper batch per GPU), total = n * world;
+    strong: a global batch of n instances split floor(r n / W), total = n."""
+    if scaling == "weak":
+        lo, hi = weak_range(rank, world, n)
+        return lo, hi, n * world
+    if scaling == "strong":
+        lo, hi = strong_range(rank, world, n)
+        return lo, hi, n
+    raise ValueError("scaling must be 'weak' or 'strong'")
+
+
+def checksum(t) -> int:
+    """Wrapping 64-bit sum of a limb tensor's bytes read as int64 words (any
+    device).  Additive over row ranges, so the sum of the per-rank checksums
+    (mod 2^64) equals the single-GPU checksum of the same global rows."""
+    import torch
+    flat = t.contiguous().view(-1)
+    if flat.dtype != torch.int64:
+        flat = flat.view(torch.int32)
+        if flat.numel() % 2:
+            flat = torch.cat([flat, flat.new_zeros(1)])
+        flat = flat.view(torch.int64)
+    return int(flat.sum().item()) & ((1 << 64) - 1)
+
+
+def combine_checksums(parts) -> int:
+    """Global checksum from per-rank ones (mod 2^64)."""
+    return sum(int(p) for p in parts) & ((1 << 64) - 1)
+
+
+def gather_objects(obj, dist=None):
+    """All ranks' `obj` in rank order (a list of one at world size 1)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out

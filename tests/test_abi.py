@@ -159,3 +159,12 @@ def test_wide_validation_before_launch(lib, op):
     if op == "bn_mul_wide_ntt":
         assert _call(lib, op, O, A, B, 4, 8192, 32) == 2    # 256K-bit inputs: NTT wide unsupported
     assert lib.bn_launches_per_call(7, 262144) == 0 and lib.bn_launches_per_call(6, 262144) == 1
+
+
+def test_build_stamp_tracks_flags():
+    """the in-tree library is reused only when the stamp (sources
+    + full nvcc command) matches; other flags never count as up to date."""
+    from paper_2405_14642_b200 import _build
+    _build.build()
+    assert _build.up_to_date()
+    assert not _build.up_to_date(_build.LIB, extra=("-DBN_SOME_VARIANT=1",))

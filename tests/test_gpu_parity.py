@@ -411,15 +411,14 @@ def test_wide_grid_cap_and_u64(bits, cap):
             assert np.array_equal(inputs.to_numpy_u32(got), want), f.__name__ + " u64"
     finally:
         bn.debug_set_grid_cap(0)
-    with pytest.raises(bn.BnError):  # out may not overlap an input
-        big = torch.empty((77, 3 * m), dtype=torch.int32, device=DEV)
-        x = big[:, :m].contiguous()
-        bn._wide("bn_mul_wide_classical", da, db, out=None)  # fine
-        lib = bn.load()
-        st = lib.bn_mul_wide_classical(big.data_ptr(), big.data_ptr(), db.data_ptr(), 77, m, 32, None)
-        if st != 0:
-            raise bn.BnError(st, "alias")
-        del x
+    # out (2m limbs per instance) may not overlap an input: the C ABI
+    # rejects it before any launch
+    lib = bn.load()
+    big = torch.empty((77, 3 * m), dtype=torch.int32, device=DEV)
+    st = lib.bn_mul_wide_classical(big.data_ptr(), big.data_ptr(), db.data_ptr(), 77, m, 32, None)
+    assert st == 4  # BN_EALIAS
+    st = lib.bn_mul_wide_ntt(big.data_ptr(), da.data_ptr(), big.data_ptr(), 77, m, 32, None)
+    assert st == 4
 
 
 def test_wide_full_size_4096():
@@ -509,3 +508,50 @@ def test_cluster_grid_cap(cap):
     assert _first_bad(ga, O.add(an, bnp)) is None
     assert _first_bad(gm, wm) is None
     assert _first_bad(gc, wm) is None
+
+
+@pytest.mark.parametrize("bits", CLUSTER_SIZES)
+def test_in_place_cluster_sizes(bits):
+    """out == a, out == b and a == b == out at the cluster sizes (one
+    instance per 2 / 4-CTA cluster): every CTA reads its slice before the
+    cluster scan and writes it after (include/bn.h ALIASING AND ORDER)."""
+    m = bits // 32
+    a, b = inputs.make_operands(3, m, seed=5, cls="MIX")
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    ops = [("add", bn.add, O.add), ("mul_ntt", bn.mul_ntt, O.mul)]
+    if bits <= bn.max_bits("mul_classical"):
+        ops.append(("mul_classical", bn.mul_classical, O.mul))
+    for name, f, ref in ops:
+        da, db = a.to(DEV), b.to(DEV)
+        f(da, db, out=da)
+        assert np.array_equal(inputs.to_numpy_u32(da), ref(an, bnp)), name + " out=a"
+        da = a.to(DEV)
+        f(da, db, out=db)
+        assert np.array_equal(inputs.to_numpy_u32(db), ref(an, bnp)), name + " out=b"
+        da = a.to(DEV)
+        f(da, da, out=da)
+        assert np.array_equal(inputs.to_numpy_u32(da), ref(an, an)), name + " a=b=out"
+
+
+@pytest.mark.parametrize("bits", [4096, 32768, 262144])
+def test_in_place_fused(bits):
+    """6-Add and Poly (both multiplications) in place at 4K bits and above:
+    out == a, out == b, a == b == out."""
+    m = bits // 32
+    n = {4096: 37, 32768: 5, 262144: 2}[bits]
+    a, b = inputs.make_operands(n, m, seed=11, cls="MIX")
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    ops = [("add6", lambda x, y, out: bn.add6(x, y, out=out), O.add6)]
+    for name in ("poly_classical", "poly_ntt"):
+        f = getattr(bn, name)
+        ops.append((name, lambda x, y, out, f=f: f(x, y, out=out), O.poly))
+    for name, f, ref in ops:
+        da, db = a.to(DEV), b.to(DEV)
+        f(da, db, out=da)
+        assert np.array_equal(inputs.to_numpy_u32(da), ref(an, bnp)), name + " out=a"
+        da = a.to(DEV)
+        f(da, db, out=db)
+        assert np.array_equal(inputs.to_numpy_u32(db), ref(an, bnp)), name + " out=b"
+        da = a.to(DEV)
+        f(da, da, out=da)
+        assert np.array_equal(inputs.to_numpy_u32(da), ref(an, an)), name + " a=b=out"

@@ -85,3 +85,50 @@ def test_generator_shard_invariance():
     for (lo, hi) in [(0, 13), (13, 50), (50, 100)]:
         a, b = inputs.make_operands(hi - lo, 32, seed=3, cls="MIX", inst0=lo)
         assert torch.equal(a, full_a[lo:hi]) and torch.equal(b, full_b[lo:hi])
+
+
+def _torchrun(args, world, timeout=300):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py")] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    import json
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_bench_dry_run_world2(scaling):
+    """bench.py's own rank plumbing under torchrun, world 2, gloo, no GPU:
+    shard plan (n = 37, not divisible by 2), per-rank checksums gathered to
+    rank 0, max over ranks.  The gathered checksums must equal those of the
+    same global rows generated in one process."""
+    n, bits = 37, 2048
+    line = _torchrun(["--dry-run", "--scaling", scaling, "--n-inst", str(n), "--bits", str(bits),
+                      "--cls", "MIX", "--seed", "4"], world=2)
+    m = bits // 32
+    assert line["n_gpus"] == 2 and line["max_over_ranks"] == 2.0
+    ranges = [tuple(p["range"]) for p in line["per_rank"]]
+    want_ranges = [shard.plan(r, 2, n, scaling)[:2] for r in range(2)]
+    assert ranges == want_ranges
+    total = n if scaling == "strong" else 2 * n
+    assert line["global_instances"] == total
+    a, b = inputs.make_operands(total, m, seed=4, cls="MIX")
+    for p in line["per_rank"]:
+        lo, hi = p["range"]
+        assert p["ck_a"] == shard.checksum(a[lo:hi]) and p["ck_b"] == shard.checksum(b[lo:hi])
+    assert line["global_ck_a"] == shard.checksum(a)
+    assert line["global_ck_b"] == shard.checksum(b)
+
+
+def test_checksum_additive():
+    a, _ = inputs.make_operands(37, 32, seed=9, cls="U")
+    parts = [shard.checksum(a[lo:hi]) for lo, hi in [shard.strong_range(r, 3, 37) for r in range(3)]]
+    assert shard.combine_checksums(parts) == shard.checksum(a)
+    with pytest.raises(ValueError):
+        shard.plan(0, 2, 10, "bogus")
