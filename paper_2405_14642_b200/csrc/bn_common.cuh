@@ -99,6 +99,22 @@ BN_DEV void sts_limbs(uint32_t* dst, const uint32_t (&r)[L]) {
     reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
 }
 
+// Shared-memory swizzle for arrays accessed as Q consecutive words per
+// thread with 128-bit accesses (Q = 8 or 16) and also, in some kernels, in a
+// pass layout (consecutive threads -> consecutive words): XOR the 16-byte
+// chunk index inside each 32-word row with the row number's low bits.  A
+// permutation inside every aligned 16-word group; the 8 threads of a
+// quarter-warp then hit 8 distinct 16-byte bank groups instead of Q/4-way
+// conflicts (tests/test_ntt_layout.py::test_epilogue_swizzle_conflict_free).
+// S = false: plain row-major (kernels whose issue slots are the binding limit
+// measured faster without the extra address arithmetic).
+template <int Q, bool S = true>
+BN_DEV int cswz(int k) {
+  static_assert(Q == 8 || Q == 16, "Q words per thread");
+  if constexpr (S) return k ^ (((k >> 5) & (Q / 4 - 1)) << 2);
+  else return k;
+}
+
 // cp.async (LDGSTS) 16-byte global -> shared copy; !valid zero-fills the
 // destination without reading the source.
 BN_DEV void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
@@ -155,9 +171,9 @@ BN_DEV uint32_t inc4_cc(uint32_t (&s)[4], uint32_t cin) {
 
 template <int L>
 BN_DEV void chunk_sum(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&s)[L], uint32_t& g,
-                      uint32_t& p) {
+                      uint32_t& p, uint32_t cin = 0) {
   static_assert(L % 4 == 0, "L must be a multiple of 4");
-  uint32_t c = 0, all = 0xFFFFFFFFu;
+  uint32_t c = cin, all = 0xFFFFFFFFu;
 #pragma unroll
   for (int v = 0; v < L / 4; v++) {
     uint32_t t[4];
@@ -296,6 +312,26 @@ BN_DEV void add_regs(const uint32_t (&x)[L], const uint32_t (&y)[L], uint32_t (&
   if (!valid) g = p = 0;
   uint32_t cin = carry_scan<TPI>(g, p, agg);
   chunk_apply<L>(x, r, cin);
+}
+
+// Carry-save chaining of consecutive additions r_k = r_{k-1} + z_k (the
+// fused 6-Add): addition k is left pending as (s, cin, p) — the chunk sum,
+// the chunk's carry-in from its scan, the chunk's all-ones flag — and its
+// final increment r_k = s + cin is folded into the NEXT addition's carry
+// chain as that chain's carry-in, so every addition but the last costs one
+// L-limb carry chain instead of two.  The fold counts a carry twice in one
+// case only: s all ones and cin = 1 (r_k's chunk is 0, its carry already
+// went to the chunk above through addition k's scan); then the next chain's
+// carry-out is cleared.  Each addition is still a full §2 carry scan.
+template <int L, int TPI>
+BN_DEV void add_pending(uint32_t (&s)[L], const uint32_t (&z)[L], uint32_t& cin, uint32_t& p, bool valid,
+                        uint32_t* agg) {
+  const uint32_t ov = p & cin;
+  uint32_t g;
+  chunk_sum<L>(s, z, s, g, p, cin);
+  g &= ~ov;
+  if (!valid) g = p = 0;
+  cin = carry_scan<TPI>(g, p, agg);
 }
 
 // r += y in place (the fused 6-Add accumulator: one limb set fewer live

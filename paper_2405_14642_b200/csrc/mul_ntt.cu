@@ -44,8 +44,19 @@ namespace cg = cooperative_groups;
 #ifndef BN_NTT_TT_MAXLOG
 #define BN_NTT_TT_MAXLOG 12  // A/B: 16K -9.4%, 32K -7.7% vs 256-thread CTAs
 #endif
-// the Poly kernel keeps 256-thread CTAs (64 measured 26% slower for it)
-constexpr int kPolyNttTT = 256;
+// target CTA size of the 16-element Poly kernel
+#ifndef BN_POLY_NTT_TT
+#define BN_POLY_NTT_TT 256
+#endif
+constexpr int kPolyNttTT = BN_POLY_NTT_TT;
+// smallest log2 N whose Poly runs on the 32-element layout
+#ifndef BN_POLY_R32_MIN
+#define BN_POLY_R32_MIN 13
+#endif
+// Poly on the 32-element layout: forward-transform a and b one at a time
+#ifndef BN_POLY_R32_SEQ
+#define BN_POLY_R32_SEQ 0
+#endif
 // residency target (threads per SM) of the 16-element kernel for N <= 256.
 // A/B at 4K (ms): 768 -> 2.882 (80 registers), 896 -> 2.891 (72), 1024 ->
 // 2.921 (64; shared memory caps all three at 12-14 CTAs of 64 threads)
@@ -320,30 +331,129 @@ BN_DEV void add3(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t c0, uint32_t
       : "r"(c0), "r"(c1), "r"(c2));
 }
 
-// ------------------------------------------------------------ one product
-// out = x * y (+ addend) mod 2^bits for this slot's instance: per prime
-// N-1..N-4, then CRT / publish (N-5, N-6), resolve (N-7) and, when ADD, a
-// second scan-add of the addend fused into the epilogue (the Poly workload).
-// SQ: x == y, so one forward transform serves both operands (Â * Â).
-// XWS / AWS / OWS: operand / addend / destination live in the in-kernel
-// workspace (coherent ld.global.cg, write-back stores) instead of HBM
-// (ld.global.nc, streaming stores).  Ends with a CTA barrier.
-template <int LOGN, bool SQ, bool ADD, bool XWS, bool AWS, bool OWS, int TTA = kPolyNttTT>
-BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const uint32_t* yi,
-                        const uint32_t* addi, uint32_t* dsti, bool valid, const uint2* __restrict__ tw) {
-  using C = NttCfg<LOGN, TTA>;
-  constexpr int N = C::N, M = C::M, TPI = C::TPI;
-  // this slot's own (padded) exchange region, reused for L | H after the
-  // transforms: it must not reach into another slot's region, because slots
-  // in different warps only synchronise at CTA barriers
-  uint32_t* X = sm + slot * (C::XW / C::IPB);
-  // raw inverse outputs per prime; per-slot stride padded by 16 words so the two
-  // instances sharing a warp (TPI = 16) write different banks
-  constexpr int RS = 3 * M + (C::TPI < 32 ? 16 : 0);
-  uint32_t* Res = sm + 2 * C::XW + slot * RS;
-  uint32_t* agg = sm + 2 * C::XW + C::IPB * RS;
-  constexpr int NV = SQ ? 1 : 2;
+// ------------------------------------------------------------ epilogue layout
+// Residue arrays are written in a pass layout (consecutive threads ->
+// consecutive words) and read back as Q consecutive words per thread with
+// 128-bit accesses; the L / H arrays are written and read Q words per
+// thread.  Row-major, the 8 threads of a quarter-warp access 16-byte chunks
+// 4Q bytes apart: a 2-way (Q = 8) or 4-way (Q = 16) bank conflict (ncu r02:
+// 14% of the shared wavefronts at 4K, 22% at 128K / 256K).  The Q = 16
+// kernels (32-element, wide, cluster32) use the cswz<16> layout
+// (bn_common.cuh): A/B on B200 (ms per paper batch) wide 4K 3.42 -> 3.23,
+// 16K 4.52 -> 4.35, 128K 7.34 -> 7.11; mul_ntt 256K 6.53 -> 6.45.  The
+// Q = 8 16-element kernels keep the plain layout (S = false): there the
+// issue slots are the binding limit and the swizzle's address arithmetic
+// cost more than the 2-way conflicts (4K 2.873 -> 2.904, 16K 3.81 -> 3.86).
+// NW words at logical index k0 (a multiple of 4) of a cswz<Q> array
+template <int Q, int NW, bool S = true>
+BN_DEV void lds_swz(uint32_t (&r)[NW], const uint32_t* base, int k0) {
+#pragma unroll
+  for (int v = 0; v < NW / 4; v++) {
+    const uint4 x = *reinterpret_cast<const uint4*>(base + cswz<Q, S>(k0 + 4 * v));
+    r[4 * v + 0] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+  }
+}
+template <int Q, int NW, bool S = true>
+BN_DEV void sts_swz(uint32_t* base, int k0, const uint32_t (&r)[NW]) {
+#pragma unroll
+  for (int v = 0; v < NW / 4; v++)
+    *reinterpret_cast<uint4*>(base + cswz<Q, S>(k0 + 4 * v)) =
+        make_uint4(r[4 * v + 0], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+}
 
+// N-5 / N-6: Garner CRT (reading R10) of the Q consecutive coefficients
+// k0 .. k0+Q-1, read from the three residue arrays Res + j RS (cswz<Q>
+// layout), with the inverse-transform scale 2^32 N^-1 folded into the
+// constants, then aggregated: S = sum_q c_{k0+q} 2^(32 q) -> lows[q] = limb q
+// of S, (h0, h1) = the two words above it (S >> 32Q < 2^46).
+//   r0 = y0 K0 mod p0
+//   t1 = (y1 K1 - r0) p0^-1 mod p1
+//   t2 = (y2 K2 - r0 - p0 t1) (p0 p1)^-1 mod p2
+//   c  = r0 + p0 t1 + p0 p1 t2  (< 2^90; c < m (2^32-1)^2 exactly)
+// G: the residues are in global memory (the Poly kernel's workspace, written
+// in this kernel: coherent ld.global.cg, row-major) instead of shared memory.
+template <int Q, bool S, bool G = false>
+BN_DEV void crt_aggregate(const uint32_t* Res, int RS, int k0, const CrtConst& k, uint32_t (&lows)[Q],
+                          uint32_t& h0, uint32_t& h1) {
+  const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
+  uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+  for (int h = 0; h < Q / 8; h++) {
+    uint32_t y0[8], y1[8], y2[8];
+    if constexpr (G) {
+      ldcg_limbs<8>(y0, Res + 0 * RS + k0 + 8 * h);
+      ldcg_limbs<8>(y1, Res + 1 * RS + k0 + 8 * h);
+      ldcg_limbs<8>(y2, Res + 2 * RS + k0 + 8 * h);
+    } else {
+      lds_swz<Q, 8, S>(y0, Res + 0 * RS, k0 + 8 * h);
+      lds_swz<Q, 8, S>(y1, Res + 1 * RS, k0 + 8 * h);
+      lds_swz<Q, 8, S>(y2, Res + 2 * RS, k0 + 8 * h);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
+      const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
+      const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
+      const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
+      const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
+      const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
+      const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
+      const uint32_t d = red2(b2v + c2v, 2 * p2);
+      const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
+      const uint64_t v64 = (uint64_t)p0 * t1 + r0;
+      const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+      const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
+      add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
+      lows[8 * h + q] = a0;
+      a0 = a1;
+      a1 = a2;
+      a2 = 0;
+    }
+  }
+  h0 = a0;
+  h1 = a1;
+}
+
+// Publish (reading R8, as the classical kernel): L[k0 .. k0+Q) = lows,
+// H[k0+Q] = h0, H[k0+Q+1] = h1, H[k0+Q+2 .. k0+2Q) = 0; the top chunk
+// (k0 + Q == M) zeroes H[0 .. Q) instead (positions >= M are dropped).
+// L and H are cswz<Q> arrays of M words.
+template <int Q, bool S>
+BN_DEV void publish_lh(uint32_t* L, uint32_t* H, int k0, int M, const uint32_t (&lows)[Q], uint32_t h0,
+                       uint32_t h1) {
+  uint32_t hs[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) hs[q] = q == 0 ? h0 : (q == 1 ? h1 : 0u);
+  sts_swz<Q, Q, S>(L, k0, lows);
+  if (k0 + Q < M) {
+    sts_swz<Q, Q, S>(H, k0 + Q, hs);
+  } else {
+#pragma unroll
+    for (int q = 0; q < Q; q++) hs[q] = 0;
+    sts_swz<Q, Q, S>(H, 0, hs);
+  }
+}
+
+// ------------------------------------------------------------ one product
+// The pieces of one NTT product for one instance slot of the 16-element
+// layout, used by the fused Poly kernel:
+//  * ntt_residues: per prime N-1..N-4 — reduce, forward transform(s),
+//    pointwise product, inverse — leaving the raw inverse outputs of
+//    coefficients 0..M-1 in Res[j M + k] (three arrays of M words);
+//  * ntt_epilogue: N-5..N-7 — Garner CRT + aggregate + L / H publish (into
+//    the slot's exchange region X), resolve R = L + H by the scan-add and,
+//    when ADD, a second scan-add of the addend (the Poly additions fused into
+//    the product's epilogue), then the store.
+// SQ: x == y, one forward transform serves both operands (x-hat * x-hat).
+// XWS / AWS / OWS: operand / addend / destination in the in-kernel workspace
+// (coherent ld.global.cg, write-back stores) instead of HBM (ld.global.nc,
+// streaming stores).
+template <int LOGN, bool SQ, bool XWS, int TTA>
+BN_DEV void ntt_residues(uint32_t* sm, int slot, int t, const uint32_t* xi, const uint32_t* yi, uint32_t* Res,
+                         bool valid, const uint2* __restrict__ tw) {
+  using C = NttCfg<LOGN, TTA>;
+  constexpr int N = C::N, M = C::M;
+  constexpr int NV = SQ ? 1 : 2;
 #pragma unroll 1
   for (int j = 0; j < kNumPrimes; j++) {
     const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
@@ -381,60 +491,26 @@ BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const
 #pragma unroll
     for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
   }
-  bar<TPI>();
+}
 
+template <int LOGN, bool ADD, bool AWS, bool OWS, int TTA>
+BN_DEV void ntt_epilogue(uint32_t* X, const uint32_t* Res, uint32_t* agg, int t, bool valid, const uint32_t* addi,
+                         uint32_t* dsti) {
+  using C = NttCfg<LOGN, TTA>;
+  constexpr int M = C::M, TPI = C::TPI;
+  bar<TPI>();  // residues complete; X dead (its last readers were the final exchange)
   // N-5 / N-6: Garner CRT of 8 consecutive coefficients, aggregate, publish
   {
-    const CrtConst& k = c_crt[LOGN];
-    const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-    uint32_t y0[8], y1[8], y2[8];
-    lds_limbs<8>(y0, Res + 0 * M + 8 * t);
-    lds_limbs<8>(y1, Res + 1 * M + 8 * t);
-    lds_limbs<8>(y2, Res + 2 * M + 8 * t);
-    uint32_t lows[8], hs[8];
-    uint32_t a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-      const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-      const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-      const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-      const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-      const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-      const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-      const uint32_t d = red2(b2v + c2v, 2 * p2);
-      const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-      // c = r0 + p0 t1 + p0 p1 t2  (< 2^90)
-      const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-      const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-      const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
-      add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
-      lows[q] = a0;
-      a0 = a1;
-      a1 = a2;
-      a2 = 0;
-    }
-#pragma unroll
-    for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
-    // X is dead (last exchange read it before inv_pass<0>, followed by bar)
-    uint32_t* L = X;
-    uint32_t* H = X + M;
-    sts_limbs<8>(L + 8 * t, lows);
-    if (8 * t + 8 < M) {
-      sts_limbs<8>(H + 8 * t + 8, hs);
-    } else {
-      uint32_t z[8];
-#pragma unroll
-      for (int q = 0; q < 8; q++) z[q] = 0;
-      sts_limbs<8>(H, z);
-    }
+    uint32_t lows[8], h0, h1;
+    crt_aggregate<8, false>(Res, M, 8 * t, c_crt[LOGN], lows, h0, h1);
+    publish_lh<8, false>(X, X + M, 8 * t, M, lows, h0, h1);
   }
   bar<TPI>();
   // N-7: R = L + H (+ addend), store
   {
     uint32_t xl[8], yh[8], r[8];
-    lds_limbs<8>(xl, X + 8 * t);
-    lds_limbs<8>(yh, X + M + 8 * t);
+    lds_swz<8, 8, false>(xl, X, 8 * t);
+    lds_swz<8, 8, false>(yh, X + M, 8 * t);
     add_regs<8, TPI>(xl, yh, r, valid, agg);
     if constexpr (ADD) {
       uint32_t ad[8], r2[8];
@@ -451,6 +527,54 @@ BN_DEV void ntt_product(uint32_t* sm, int slot, int t, const uint32_t* xi, const
     }
   }
   __syncthreads();  // X / Res / agg reused next; dst visible to the CTA
+}
+
+// Poly's first level, transform-shared: per prime, the forward transforms
+// A-hat, B-hat are computed once (together), then the three pointwise
+// products A-hat^2, B-hat^2, A-hat B-hat are inverse-transformed one after
+// the other into Res9[(3 P + j) M + k] (P = 0: a*a, 1: b*b, 2: a*b).
+// A-hat stays in registers; B-hat is parked in the slot's plane-1 region,
+// which the one-vector inverse exchanges never touch (thread-private slots
+// [e TPI + t]: only the owner reads them back, no barrier needed).
+template <int LOGN, int TTA>
+BN_DEV void ntt_residues3(uint32_t* sm, int slot, int t, const uint32_t* ai, const uint32_t* bi, uint32_t* Res9,
+                          bool valid, const uint2* __restrict__ tw) {
+  using C = NttCfg<LOGN, TTA>;
+  constexpr int N = C::N, M = C::M, TPI = C::TPI;
+  uint32_t* Bp = sm + C::XW + slot * (C::XW / C::IPB);  // plane 1 of this slot
+#pragma unroll 1
+  for (int j = 0; j < kNumPrimes; j++) {
+    const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+    const uint2* twf = tw + (2 * j + 0) * (N - 1);
+    const uint2* twi = tw + (2 * j + 1) * (N - 1);
+    uint32_t xab[2][16];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const uint32_t va = valid ? __ldg(ai + t + e * (N / 16)) : 0u;
+      const uint32_t vb = valid ? __ldg(bi + t + e * (N / 16)) : 0u;
+      xab[0][e] = red2(red2(va, p2), p2);
+      xab[1][e] = red2(red2(vb, p2), p2);
+    }
+#pragma unroll
+    for (int e = 8; e < 16; e++) xab[0][e] = xab[1][e] = 0u;
+    fwd_all<LOGN, true, 2, TTA>(xab, sm, slot * N, t, twf, p, p2);
+    bar<TPI>();  // every read of plane 1 by the last forward exchange is done
+#pragma unroll
+    for (int e = 0; e < 16; e++) Bp[e * TPI + t] = xab[1][e];
+    uint32_t(&ah)[16] = xab[0];
+#pragma unroll 1
+    for (int P = 0; P < 3; P++) {
+      uint32_t x[16];
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        const uint32_t bh = P == 0 ? 0u : Bp[e * TPI + t];
+        x[e] = mont(P == 1 ? bh : ah[e], P == 0 ? ah[e] : bh, p, pinv);
+      }
+      inv_all<LOGN, TTA>(x, sm, slot * N, t, twi, p, p2);
+#pragma unroll
+      for (int e = 0; e < 8; e++) Res9[(3 * P + j) * M + t + e * (N / 16)] = x[e];
+    }
+  }
 }
 
 // ------------------------------------------------------------ the kernels
@@ -511,62 +635,23 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
       inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
       // keep coefficients 0..M-1 (truncated product): e < 8
 #pragma unroll
-      for (int e = 0; e < 8; e++) Res[j * M + t + e * (N / 16)] = x[e];
+      for (int e = 0; e < 8; e++) Res[j * M + cswz<8, false>(t + e * (N / 16))] = x[e];
     }
     bar<TPI>();
 
     // N-5 / N-6: Garner CRT of 8 consecutive coefficients, aggregate, publish
+    // (X is dead: the last exchange read it before inv_pass<0>, then bar)
     {
-      const CrtConst& k = c_crt[LOGN];
-      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-      uint32_t y0[8], y1[8], y2[8];
-      lds_limbs<8>(y0, Res + 0 * M + 8 * t);
-      lds_limbs<8>(y1, Res + 1 * M + 8 * t);
-      lds_limbs<8>(y2, Res + 2 * M + 8 * t);
-      uint32_t lows[8], hs[8];
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-        const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-        const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-        const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-        const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-        const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-        const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-        const uint32_t d = red2(b2v + c2v, 2 * p2);
-        const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-        // c = r0 + p0 t1 + p0 p1 t2  (< 2^90)
-        const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-        const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-        const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
-        add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
-        lows[q] = a0;
-        a0 = a1;
-        a1 = a2;
-        a2 = 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
-      // X is dead (last exchange read it before inv_pass<0>, followed by bar)
-      uint32_t* L = X;
-      uint32_t* H = X + M;
-      sts_limbs<8>(L + 8 * t, lows);
-      if (8 * t + 8 < M) {
-        sts_limbs<8>(H + 8 * t + 8, hs);
-      } else {
-        uint32_t z[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) z[q] = 0;
-        sts_limbs<8>(H, z);
-      }
+      uint32_t lows[8], h0, h1;
+      crt_aggregate<8, false>(Res, M, 8 * t, c_crt[LOGN], lows, h0, h1);
+      publish_lh<8, false>(X, X + M, 8 * t, M, lows, h0, h1);
     }
     bar<TPI>();
     // N-7: R = L + H, store
     {
       uint32_t xl[8], yh[8], r[8];
-      lds_limbs<8>(xl, X + 8 * t);
-      lds_limbs<8>(yh, X + M + 8 * t);
+      lds_swz<8, 8, false>(xl, X, 8 * t);
+      lds_swz<8, 8, false>(yh, X + M, 8 * t);
       add_regs<8, TPI>(xl, yh, r, valid, agg);
       if (valid) store_limbs<8>(out + inst * M + 8 * t, r);
     }
@@ -576,20 +661,38 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttCfg<LOGN>::MINB)
 
 // Poly (Table 2 caption): (a*a + b) * (b*b + b) + a*b
 // mod 2^bits in ONE kernel — four NTT products with the three additions
-// fused into their epilogues (block-level fusion).  a^2 and b^2 each need a
-// single forward transform (SQ), so a group costs 10 transforms per prime
-// instead of 12.  The intermediates t1 = a^2 + b, t2 = b^2 + b, t3 = a b go
-// to this CTA's private workspace slice (L2-resident, rewritten by the same
-// CTA group after group) and are read back coherently by the last product.
+// fused into their epilogues (block-level fusion).  The three first-level
+// products share their forward transforms (ntt_residues3): per prime
+// 2 forward + 3 inverse transforms, then t1 * t2 costs 2 + 1, so a Poly is
+// 8 transforms per prime (four independent products: 12; squaring reuse
+// alone: 10).  The residues of the first level (9 M words per instance)
+// stay in shared memory; t1 = a^2 + b, t2 = b^2 + b, t3 = a b go to this
+// CTA's private workspace slice (L2-resident, rewritten by the same CTA group
+// after group) and are read back coherently by the last product.
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN, kPolyNttTT>::T, NttCfg<LOGN, kPolyNttTT>::MINB)
+struct PolyNttCfg {
+  using B = NttCfg<LOGN, kPolyNttTT>;
+  static constexpr int RS = 9 * B::M + (B::TPI < 32 ? 16 : 0);  // per slot: [3 P + j][M]
+  static constexpr int SMEM_WORDS = 2 * B::XW + B::IPB * RS + B::T / 32;
+  // residency the shared memory allows (227 KiB per SM): never ask ptxas to
+  // cap registers for CTAs that could not be co-resident anyway
+  static constexpr int BY_SMEM = (227 * 1024) / (SMEM_WORDS * 4);
+  static constexpr int MINB = BY_SMEM < 1 ? 1 : (BY_SMEM < B::MINB ? BY_SMEM : B::MINB);
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN, kPolyNttTT>::T, PolyNttCfg<LOGN>::MINB)
     poly_ntt_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                     const uint2* __restrict__ tw, uint32_t* ws) {
   using C = NttCfg<LOGN, kPolyNttTT>;
+  using PC = PolyNttCfg<LOGN>;
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   const int slot = threadIdx.x / C::TPI;
   const int t = threadIdx.x % C::TPI;
+  uint32_t* X = sm + slot * (C::XW / C::IPB);
+  uint32_t* Res9 = sm + 2 * C::XW + slot * PC::RS;
+  uint32_t* agg = sm + 2 * C::XW + C::IPB * PC::RS;
   uint32_t* t1 = ws + ((uint64_t)blockIdx.x * C::IPB + slot) * 3 * M;
   uint32_t* t2 = t1 + M;
   uint32_t* t3 = t2 + M;
@@ -600,11 +703,15 @@ __global__ void __launch_bounds__(NttCfg<LOGN, kPolyNttTT>::T, NttCfg<LOGN, kPol
     const uint64_t io = (valid ? inst : 0) * M;
     const uint32_t* ai = a + io;
     const uint32_t* bi = b + io;
-    //                 SQ     ADD    XWS    AWS    OWS
-    ntt_product<LOGN, true, true, false, false, true>(sm, slot, t, ai, ai, bi, t1, valid, tw);
-    ntt_product<LOGN, true, true, false, false, true>(sm, slot, t, bi, bi, bi, t2, valid, tw);
-    ntt_product<LOGN, false, false, false, false, true>(sm, slot, t, ai, bi, nullptr, t3, valid, tw);
-    ntt_product<LOGN, false, true, true, true, false>(sm, slot, t, t1, t2, t3, out + io, valid, tw);
+    constexpr int TT = kPolyNttTT;
+    ntt_residues3<LOGN, TT>(sm, slot, t, ai, bi, Res9, valid, tw);
+    //               ADD    AWS    OWS
+    ntt_epilogue<LOGN, true, false, true, TT>(X, Res9 + 0 * M, agg, t, valid, bi, t1);   // a^2 + b
+    ntt_epilogue<LOGN, true, false, true, TT>(X, Res9 + 3 * M, agg, t, valid, bi, t2);   // b^2 + b
+    ntt_epilogue<LOGN, false, false, true, TT>(X, Res9 + 6 * M, agg, t, valid, nullptr, t3);  // a b
+    //                SQ     XWS
+    ntt_residues<LOGN, false, true, TT>(sm, slot, t, t1, t2, Res9, valid, tw);
+    ntt_epilogue<LOGN, true, true, false, TT>(X, Res9, agg, t, valid, t3, out + io);  // t1 t2 + t3
   }
 }
 
@@ -715,63 +822,21 @@ __global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
       xchg32<L1, L0, 1, N>(x, X, t);
       inv_pass<LOGN, 0, 32>(x[0], t, twi, p, p2);
 #pragma unroll
-      for (int e = 0; e < 16; e++) Res[j * M + t + e * (N / 32)] = x[0][e];
+      for (int e = 0; e < 16; e++) Res[j * M + cswz<16>(t + e * (N / 32))] = x[0][e];
     }
     __syncthreads();
 
     // N-5 / N-6: Garner CRT of 16 consecutive coefficients, aggregate, publish
     {
-      const CrtConst& k = c_crt[LOGN];
-      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-      uint32_t lows[16];
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        uint32_t y0[8], y1[8], y2[8];
-        lds_limbs<8>(y0, Res + 0 * M + 16 * t + 8 * h);
-        lds_limbs<8>(y1, Res + 1 * M + 16 * t + 8 * h);
-        lds_limbs<8>(y2, Res + 2 * M + 16 * t + 8 * h);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-          const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-          const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-          const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-          const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-          const uint32_t d = red2(b2v + c2v, 2 * p2);
-          const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-          const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
-          add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
-          lows[8 * h + q] = a0;
-          a0 = a1;
-          a1 = a2;
-          a2 = 0;
-        }
-      }
-      uint32_t hs[16];
-#pragma unroll
-      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
-      uint32_t* L = X;
-      uint32_t* H = X + N;
-      sts_limbs<16>(L + 16 * t, lows);
-      if (16 * t + 16 < M) {
-        sts_limbs<16>(H + 16 * t + 16, hs);
-      } else {
-        uint32_t z[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) z[q] = 0;
-        sts_limbs<16>(H, z);
-      }
+      uint32_t lows[16], h0, h1;
+      crt_aggregate<16, true>(Res, M, 16 * t, c_crt[LOGN], lows, h0, h1);
+      publish_lh<16, true>(X, X + N, 16 * t, M, lows, h0, h1);
     }
     __syncthreads();
     {
       uint32_t xl[16], yh[16], r[16];
-      lds_limbs<16>(xl, X + 16 * t);
-      lds_limbs<16>(yh, X + N + 16 * t);
+      lds_swz<16, 16>(xl, X, 16 * t);
+      lds_swz<16, 16>(yh, X + N, 16 * t);
       add_regs<16, T>(xl, yh, r, true, agg);
       store_limbs<16>(out + inst * M + 16 * t, r);
     }
@@ -793,6 +858,198 @@ static cudaError_t launch_ntt_r32_t(uint32_t* out, const uint32_t* a, const uint
   const unsigned grid = cap_grid((unsigned)(n_inst < cap ? n_inst : cap));
   mul_ntt_r32_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw);
   return cudaGetLastError();
+}
+
+// Poly at N = 2^13, 2^14 (128K / 256K bits) on the 32-element layout: the
+// 16-element kernel would need 1024-thread CTAs capped at 64 registers
+// (spills) and, at 2^14, more shared memory than a CTA has for the 9 M
+// first-level residues.  Same transform sharing as poly_ntt_kernel
+// (8 transforms per prime); the first-level residues go to the CTA's
+// workspace slice in global memory (L2-resident; written coalesced in the
+// pass-0 layout, read back 16 consecutive words per thread), the last
+// product's residues stay in shared memory as in the 1-Mul kernel.
+// Workspace per resident CTA: G9 (9 M words) | t1 | t2 | t3 (M words each).
+template <int LOGN>
+struct PolyR32Cfg {
+  using B = NttR32Cfg<LOGN>;
+  static constexpr int WS_WORDS = 12 * B::M;
+};
+
+template <int LOGN>
+BN_DEV void r32_fwd(uint32_t (&xab)[2][32], uint32_t* X, int t, const uint2* twf, uint32_t p, uint32_t p2) {
+  constexpr int N = 1 << LOGN;
+  constexpr int L0 = PassCfgR<LOGN, 0, 5>::LO, L1 = PassCfgR<LOGN, 1, 5>::LO, L2 = PassCfgR<LOGN, 2, 5>::LO;
+  fwd_pass<LOGN, 0, true, 2, 32>(xab, t, twf, p, p2);
+  xchg32<L0, L1, 2, N>(xab, X, t);
+  fwd_pass<LOGN, 1, true, 2, 32>(xab, t, twf, p, p2);
+  xchg32<L1, L2, 2, N>(xab, X, t);
+  fwd_pass<LOGN, 2, true, 2, 32>(xab, t, twf, p, p2);
+}
+
+template <int LOGN>
+BN_DEV void r32_fwd1(uint32_t (&x)[1][32], uint32_t* X, int t, const uint2* twf, uint32_t p, uint32_t p2) {
+  constexpr int N = 1 << LOGN;
+  constexpr int L0 = PassCfgR<LOGN, 0, 5>::LO, L1 = PassCfgR<LOGN, 1, 5>::LO, L2 = PassCfgR<LOGN, 2, 5>::LO;
+  fwd_pass<LOGN, 0, true, 1, 32>(x, t, twf, p, p2);
+  xchg32<L0, L1, 1, N>(x, X, t);
+  fwd_pass<LOGN, 1, true, 1, 32>(x, t, twf, p, p2);
+  xchg32<L1, L2, 1, N>(x, X, t);
+  fwd_pass<LOGN, 2, true, 1, 32>(x, t, twf, p, p2);
+}
+
+template <int LOGN>
+BN_DEV void r32_inv(uint32_t (&x)[1][32], uint32_t* X, int t, const uint2* twi, uint32_t p, uint32_t p2) {
+  constexpr int N = 1 << LOGN;
+  constexpr int L0 = PassCfgR<LOGN, 0, 5>::LO, L1 = PassCfgR<LOGN, 1, 5>::LO, L2 = PassCfgR<LOGN, 2, 5>::LO;
+  inv_pass<LOGN, 2, 32>(x[0], t, twi, p, p2);
+  xchg32<L2, L1, 1, N>(x, X, t);
+  inv_pass<LOGN, 1, 32>(x[0], t, twi, p, p2);
+  xchg32<L1, L0, 1, N>(x, X, t);
+  inv_pass<LOGN, 0, 32>(x[0], t, twi, p, p2);
+}
+
+// raw limbs of x, y (16 each, pass-0 layout t + e N/32) reduced mod p
+template <int LOGN, bool XWS>
+BN_DEV void r32_load(uint32_t (&xab)[2][32], const uint32_t* xi, const uint32_t* yi, int t, uint32_t p2) {
+  constexpr int N = 1 << LOGN;
+#pragma unroll
+  for (int e = 0; e < 16; e++) {
+    const uint32_t* px = xi + t + e * (N / 32);
+    const uint32_t* py = yi + t + e * (N / 32);
+    xab[0][e] = red2(red2(XWS ? __ldcg(px) : __ldg(px), p2), p2);
+    xab[1][e] = red2(red2(XWS ? __ldcg(py) : __ldg(py), p2), p2);
+  }
+#pragma unroll
+  for (int e = 16; e < 32; e++) xab[0][e] = xab[1][e] = 0u;
+}
+
+// N-5..N-7 on the 32-element layout: CRT of 16 consecutive coefficients
+// (residues in shared memory, cswz<16>, or in global memory when G), L / H
+// publish into the planes, resolve (+ addend), store.  Brackets itself with
+// CTA barriers.
+template <int LOGN, bool G, bool ADD, bool AWS, bool OWS>
+BN_DEV void r32_epilogue(uint32_t* X, const uint32_t* Res, uint32_t* agg, int t, const uint32_t* addi,
+                         uint32_t* dsti) {
+  constexpr int N = 1 << LOGN, M = N / 2, T = N / 32;
+  __syncthreads();  // residues complete (shared or global); planes dead
+  {
+    uint32_t lows[16], h0, h1;
+    crt_aggregate<16, true, G>(Res, M, 16 * t, c_crt[LOGN], lows, h0, h1);
+    publish_lh<16, true>(X, X + N, 16 * t, M, lows, h0, h1);
+  }
+  __syncthreads();
+  {
+    uint32_t xl[16], yh[16], r[16];
+    lds_swz<16, 16>(xl, X, 16 * t);
+    lds_swz<16, 16>(yh, X + N, 16 * t);
+    add_regs<16, T>(xl, yh, r, true, agg);
+    if constexpr (ADD) {
+      uint32_t ad[16], r2[16];
+      load_any<AWS, 16>(ad, addi + 16 * t);
+      __syncthreads();  // agg reuse
+      add_regs<16, T>(r, ad, r2, true, agg);
+      store_any<OWS, 16>(dsti + 16 * t, r2);
+    } else {
+      store_any<OWS, 16>(dsti + 16 * t, r);
+    }
+  }
+  __syncthreads();  // planes / agg reused next; dst visible to the CTA
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
+    poly_ntt_r32_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                        const uint2* __restrict__ tw, uint32_t* ws) {
+  using C = NttR32Cfg<LOGN>;
+  constexpr int N = C::N, M = C::M;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* X = sm;              // plane 0 | plane 1 (N words each)
+  uint32_t* Res = sm + 2 * N;    // 3 M residues (last product), cswz<16>
+  uint32_t* agg = Res + 3 * M;   // T / 32
+  const int t = threadIdx.x;
+  uint32_t* G9 = ws + (uint64_t)blockIdx.x * PolyR32Cfg<LOGN>::WS_WORDS;  // [3 P + j][M]
+  uint32_t* t1 = G9 + 9 * M;
+  uint32_t* t2 = t1 + M;
+  uint32_t* t3 = t2 + M;
+  for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x) {
+    const uint32_t* ai = a + inst * M;
+    const uint32_t* bi = b + inst * M;
+    // first level: A-hat, B-hat once per prime, three inverse transforms
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+#if BN_POLY_R32_SEQ
+      // A and B transformed one after the other through plane 0 (32 data
+      // registers instead of 64) and parked as soon as each is done
+      {
+        uint32_t xa[1][32];
+#pragma unroll
+        for (int e = 0; e < 16; e++) xa[0][e] = red2(red2(__ldg(ai + t + e * (N / 32)), p2), p2);
+#pragma unroll
+        for (int e = 16; e < 32; e++) xa[0][e] = 0u;
+        r32_fwd1<LOGN>(xa, X, t, twf, p, p2);
+#pragma unroll
+        for (int e = 0; e < 32; e++) Res[e * C::T + t] = xa[0][e];
+#pragma unroll
+        for (int e = 0; e < 16; e++) xa[0][e] = red2(red2(__ldg(bi + t + e * (N / 32)), p2), p2);
+#pragma unroll
+        for (int e = 16; e < 32; e++) xa[0][e] = 0u;
+        r32_fwd1<LOGN>(xa, X, t, twf, p, p2);
+#pragma unroll
+        for (int e = 0; e < 32; e++) X[N + e * C::T + t] = xa[0][e];
+      }
+#else
+      uint32_t xab[2][32];
+      r32_load<LOGN, false>(xab, ai, bi, t, p2);
+      r32_fwd<LOGN>(xab, X, t, twf, p, p2);
+      // park A-hat in the (idle) residue area and B-hat in plane 1, which the
+      // one-vector inverse exchanges never touch; thread-private slots
+      // [e T + t], read back only by their owner
+      __syncthreads();  // every read of plane 1 by the last forward exchange is done
+#pragma unroll
+      for (int e = 0; e < 32; e++) {
+        Res[e * C::T + t] = xab[0][e];
+        X[N + e * C::T + t] = xab[1][e];
+      }
+#endif
+#pragma unroll 1
+      for (int P = 0; P < 3; P++) {
+        // P = 0: A-hat^2, 1: B-hat^2, 2: A-hat B-hat
+        const uint32_t* U = (P == 1 ? X + N : Res) + t;
+        const uint32_t* V = (P == 0 ? Res : X + N) + t;
+        uint32_t x[1][32];
+#pragma unroll
+        for (int e = 0; e < 32; e++) x[0][e] = mont(U[e * C::T], V[e * C::T], p, pinv);
+        r32_inv<LOGN>(x, X, t, twi, p, p2);
+        uint32_t* g = G9 + (3 * P + j) * M;
+#pragma unroll
+        for (int e = 0; e < 16; e++) g[t + e * (N / 32)] = x[0][e];
+      }
+    }
+    //                 G     ADD    AWS    OWS
+    r32_epilogue<LOGN, true, true, false, true>(X, G9 + 0 * M, agg, t, bi, t1);       // a^2 + b
+    r32_epilogue<LOGN, true, true, false, true>(X, G9 + 3 * M, agg, t, bi, t2);       // b^2 + b
+    r32_epilogue<LOGN, true, false, false, true>(X, G9 + 6 * M, agg, t, nullptr, t3);  // a b
+    // t1 * t2 + t3
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xab[2][32];
+      r32_load<LOGN, true>(xab, t1, t2, t, p2);
+      r32_fwd<LOGN>(xab, X, t, twf, p, p2);
+      uint32_t x[1][32];
+#pragma unroll
+      for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
+      r32_inv<LOGN>(x, X, t, twi, p, p2);
+#pragma unroll
+      for (int e = 0; e < 16; e++) Res[j * M + cswz<16>(t + e * (N / 32))] = x[0][e];
+    }
+    r32_epilogue<LOGN, false, true, true, false>(X, Res, agg, t, t3, out + inst * M);
+  }
 }
 
 // ------------------------------------------------------------ beyond one CTA
@@ -930,49 +1187,23 @@ __global__ void __launch_bounds__(T, NttClCfg<LOGN, T>::MINB)
 #pragma unroll
       for (int e = 0; e < 8; e++) {
         const int k = gt + e * (N / 16);
-        st_cluster(mapa_rank(smem_addr(Res + j * MS + (k & (MS - 1))), k / MS), x[e]);
+        st_cluster(mapa_rank(smem_addr(Res + j * MS + cswz<8, false>(k & (MS - 1))), k / MS), x[e]);
       }
     }
     cl.sync();  // residues in place; every plane read is done
 
     // N-5 / N-6 on this CTA's consecutive coefficients [rank MS + 8 tid, +8)
     {
-      const CrtConst& k = c_crt[LOGN];
-      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-      uint32_t y0[8], y1[8], y2[8];
-      lds_limbs<8>(y0, Res + 0 * MS + 8 * tid);
-      lds_limbs<8>(y1, Res + 1 * MS + 8 * tid);
-      lds_limbs<8>(y2, Res + 2 * MS + 8 * tid);
-      uint32_t lows[8], hs[8];
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
+      uint32_t lows[8], hs[8], h0, h1;
+      crt_aggregate<8, false>(Res, MS, 8 * tid, c_crt[LOGN], lows, h0, h1);
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-        const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-        const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-        const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-        const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-        const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-        const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-        const uint32_t d = red2(b2v + c2v, 2 * p2);
-        const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-        const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-        const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-        const uint64_t h = (uint64_t)k.p01_hi * t2 + (w >> 32);
-        add3(a0, a1, a2, (uint32_t)w, (uint32_t)h, (uint32_t)(h >> 32));
-        lows[q] = a0;
-        a0 = a1;
-        a1 = a2;
-        a2 = 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
-      // L = plane 0 [0, MS), H = plane 1 [0, MS) (planes are dead)
+      for (int q = 0; q < 8; q++) hs[q] = q == 0 ? h0 : (q == 1 ? h1 : 0u);
+      // L = plane 0 [0, MS), H = plane 1 [0, MS) (planes are dead), cswz<8>
       uint32_t* L = X0;
       uint32_t* H = X0 + C::PL;
-      sts_limbs<8>(L + 8 * tid, lows);
+      sts_swz<8, 8, false>(L, 8 * tid, lows);
       if (tid < C::T - 1) {
-        sts_limbs<8>(H + 8 * tid + 8, hs);
+        sts_swz<8, 8, false>(H, 8 * tid + 8, hs);
       } else {
         // the CTA's top chunk spills into the next CTA's H[0, 8); the
         // instance's top chunk wraps to zero CTA 0's H[0, 8)
@@ -982,15 +1213,15 @@ __global__ void __launch_bounds__(T, NttClCfg<LOGN, T>::MINB)
         }
         const uint32_t dst = mapa_rank(smem_addr(H), (rank + 1) % C::CR);
 #pragma unroll
-        for (int q = 0; q < 8; q++) st_cluster(dst + 4 * q, hs[q]);
+        for (int q = 0; q < 8; q++) st_cluster(dst + 4 * cswz<8, false>(q), hs[q]);
       }
     }
     cl.sync();
     // N-7: R = L + H across the cluster, store
     {
       uint32_t xl[8], yh[8], r[8], g, pp;
-      lds_limbs<8>(xl, X0 + 8 * tid);
-      lds_limbs<8>(yh, X0 + C::PL + 8 * tid);
+      lds_swz<8, 8, false>(xl, X0, 8 * tid);
+      lds_swz<8, 8, false>(yh, X0 + C::PL, 8 * tid);
       chunk_sum<8>(xl, yh, r, g, pp);
       const uint32_t cin = cluster_carry_scan<C::CR>(g, pp, agg, cta_agg, parity, cl);
       chunk_apply<8>(xl, r, cin);
@@ -1134,51 +1365,21 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
       for (int e = 0; e < 16; e++) {
         const int k = gt + e * (N / 32);
-        st_cluster(mapa_rank(smem_addr(Res + j * MS + (k & (MS - 1))), k / MS), x[0][e]);
+        st_cluster(mapa_rank(smem_addr(Res + j * MS + cswz<16>(k & (MS - 1))), k / MS), x[0][e]);
       }
     }
     cl.sync();
     // CRT / aggregate 16 consecutive coefficients [rank MS + 16 tid, +16)
     {
-      const CrtConst& k = c_crt[LOGN];
-      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-      uint32_t lows[16];
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
+      uint32_t lows[16], hs[16], h0, h1;
+      crt_aggregate<16, true>(Res, MS, 16 * tid, c_crt[LOGN], lows, h0, h1);
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        uint32_t y0[8], y1[8], y2[8];
-        lds_limbs<8>(y0, Res + 0 * MS + 16 * tid + 8 * h);
-        lds_limbs<8>(y1, Res + 1 * MS + 16 * tid + 8 * h);
-        lds_limbs<8>(y2, Res + 2 * MS + 16 * tid + 8 * h);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-          const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-          const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-          const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-          const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-          const uint32_t d = red2(b2v + c2v, 2 * p2);
-          const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-          const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
-          add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
-          lows[8 * h + q] = a0;
-          a0 = a1;
-          a1 = a2;
-          a2 = 0;
-        }
-      }
-      uint32_t hs[16];
-#pragma unroll
-      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
+      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? h0 : (q == 1 ? h1 : 0u);
       uint32_t* L = X0;
       uint32_t* H = X0 + PL;
-      sts_limbs<16>(L + 16 * tid, lows);
+      sts_swz<16, 16>(L, 16 * tid, lows);
       if (tid < C::T - 1) {
-        sts_limbs<16>(H + 16 * tid + 16, hs);
+        sts_swz<16, 16>(H, 16 * tid + 16, hs);
       } else {
         if (rank == C::CR - 1) {
 #pragma unroll
@@ -1186,14 +1387,14 @@ __global__ void __launch_bounds__(512, 1)
         }
         const uint32_t dst = mapa_rank(smem_addr(H), (rank + 1) % C::CR);
 #pragma unroll
-        for (int q = 0; q < 16; q++) st_cluster(dst + 4 * q, hs[q]);
+        for (int q = 0; q < 16; q++) st_cluster(dst + 4 * cswz<16>(q), hs[q]);
       }
     }
     cl.sync();
     {
       uint32_t xl[16], yh[16], r[16], g, pp;
-      lds_limbs<16>(xl, X0 + 16 * tid);
-      lds_limbs<16>(yh, X0 + PL + 16 * tid);
+      lds_swz<16, 16>(xl, X0, 16 * tid);
+      lds_swz<16, 16>(yh, X0 + PL, 16 * tid);
       chunk_sum<16>(xl, yh, r, g, pp);
       const uint32_t cin = cluster_carry_scan<C::CR>(g, pp, agg, cta_agg, parity, cl);
       chunk_apply<16>(xl, r, cin);
@@ -1299,65 +1500,23 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttWideCfg<LOGN>::MINB)
       inv_all<LOGN>(x, sm, slot * N, t, twi, p, p2);
       // all N coefficients (the last, c_{N-1}, is 0)
 #pragma unroll
-      for (int e = 0; e < 16; e++) Res[j * N + t + e * (N / 16)] = x[e];
+      for (int e = 0; e < 16; e++) Res[j * N + cswz<16>(t + e * (N / 16))] = x[e];
     }
     bar<TPI>();
 
-    // Garner CRT of 16 consecutive coefficients, aggregate, publish
+    // Garner CRT of 16 consecutive coefficients, aggregate, publish; the
+    // planes are dead (the last exchange read them before the barrier above):
+    // L = plane 0 region, H = plane 1 region, N words each
     {
-      const CrtConst& k = c_crt[LOGN];
-      const uint32_t p0 = c_pc[0].p, p1 = c_pc[1].p, p2 = c_pc[2].p;
-      uint32_t lows[16];
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        uint32_t y0[8], y1[8], y2[8];
-        lds_limbs<8>(y0, Res + 0 * N + 16 * t + 8 * h);
-        lds_limbs<8>(y1, Res + 1 * N + 16 * t + 8 * h);
-        lds_limbs<8>(y2, Res + 2 * N + 16 * t + 8 * h);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const uint32_t r0 = red2(shoup(y0[q], k.k0, k.k0_sh, p0), p0);
-          const uint32_t u = shoup(y1[q], k.k1i, k.k1i_sh, p1);
-          const uint32_t v = shoup(r0, k.i01, k.i01_sh, p1);
-          const uint32_t t1 = red2(red2(u + 2 * p1 - v, 2 * p1), p1);
-          const uint32_t a2v = shoup(y2[q], k.k2i, k.k2i_sh, p2);
-          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, p2);
-          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, p2);
-          const uint32_t d = red2(b2v + c2v, 2 * p2);
-          const uint32_t t2 = red2(red2(a2v + 2 * p2 - d, 2 * p2), p2);
-          const uint64_t v64 = (uint64_t)p0 * t1 + r0;
-          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
-          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
-          add3(a0, a1, a2, (uint32_t)w, (uint32_t)hh, (uint32_t)(hh >> 32));
-          lows[8 * h + q] = a0;
-          a0 = a1;
-          a1 = a2;
-          a2 = 0;
-        }
-      }
-      uint32_t hs[16];
-#pragma unroll
-      for (int q = 0; q < 16; q++) hs[q] = q == 0 ? a0 : (q == 1 ? a1 : 0u);
-      // planes are dead (last exchange read them before the barrier above):
-      // L = plane 0 region, H = plane 1 region, N words each
-      uint32_t* L = X;
-      uint32_t* H = X1;
-      sts_limbs<16>(L + 16 * t, lows);
-      if (16 * t + 16 < N) {
-        sts_limbs<16>(H + 16 * t + 16, hs);
-      } else {
-        uint32_t z[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) z[q] = 0;
-        sts_limbs<16>(H, z);
-      }
+      uint32_t lows[16], h0, h1;
+      crt_aggregate<16, true>(Res, N, 16 * t, c_crt[LOGN], lows, h0, h1);
+      publish_lh<16, true>(X, X1, 16 * t, N, lows, h0, h1);
     }
     bar<TPI>();
     {
       uint32_t xl[16], yh[16], r[16];
-      lds_limbs<16>(xl, X + 16 * t);
-      lds_limbs<16>(yh, X1 + 16 * t);
+      lds_swz<16, 16>(xl, X, 16 * t);
+      lds_swz<16, 16>(yh, X1, 16 * t);
       add_regs<16, TPI>(xl, yh, r, valid, agg);
       if (valid) store_limbs<16>(out + inst * N + 16 * t, r);
     }
@@ -1434,17 +1593,28 @@ static cudaError_t launch_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t
 
 template <int LOGN>
 static cudaError_t poly_ntt_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64_t* ws_words) {
-  using C = NttCfg<LOGN, kPolyNttTT>;
-  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
   static LaunchCache cache;
   int per_sm = 0;
-  cudaError_t e = resident_ctas(cache, poly_ntt_kernel<LOGN>, C::T, smem, &per_sm);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
-  const uint64_t cap = (uint64_t)n_sm * per_sm;  // one resident wave: one workspace slice each
-  *grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
-  *ws_words = (uint64_t)*grid * C::IPB * 3 * C::M;
+  if constexpr (LOGN >= BN_POLY_R32_MIN) {
+    using C = NttR32Cfg<LOGN>;
+    constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+    cudaError_t e = resident_ctas(cache, poly_ntt_r32_kernel<LOGN>, C::T, smem, &per_sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t cap = (uint64_t)n_sm * per_sm;  // one resident wave: one workspace slice each
+    *grid = cap_grid((unsigned)(n_inst < cap ? n_inst : cap));
+    *ws_words = (uint64_t)*grid * PolyR32Cfg<LOGN>::WS_WORDS;
+  } else {
+    using C = NttCfg<LOGN, kPolyNttTT>;
+    constexpr size_t smem = PolyNttCfg<LOGN>::SMEM_WORDS * sizeof(uint32_t);
+    cudaError_t e = resident_ctas(cache, poly_ntt_kernel<LOGN>, C::T, smem, &per_sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t n_groups = (n_inst + C::IPB - 1) / C::IPB;
+    const uint64_t cap = (uint64_t)n_sm * per_sm;  // one resident wave: one workspace slice each
+    *grid = cap_grid((unsigned)(n_groups < cap ? n_groups : cap));
+    *ws_words = (uint64_t)*grid * C::IPB * 3 * C::M;
+  }
   return cudaSuccess;
 }
 
@@ -1452,14 +1622,20 @@ template <int LOGN>
 static cudaError_t launch_poly_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                      const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
                                      int n_sm) {
-  using C = NttCfg<LOGN, kPolyNttTT>;
   unsigned grid = 0;
   uint64_t need = 0;
   cudaError_t e = poly_ntt_geom_t<LOGN>(n_inst, n_sm, &grid, &need);
   if (e != cudaSuccess) return e;
   if (ws_words < need) return cudaErrorInvalidValue;
-  constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
-  poly_ntt_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw, ws);
+  if constexpr (LOGN >= BN_POLY_R32_MIN) {
+    using C = NttR32Cfg<LOGN>;
+    constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+    poly_ntt_r32_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw, ws);
+  } else {
+    using C = NttCfg<LOGN, kPolyNttTT>;
+    constexpr size_t smem = PolyNttCfg<LOGN>::SMEM_WORDS * sizeof(uint32_t);
+    poly_ntt_kernel<LOGN><<<grid, C::T, smem, st>>>(out, a, b, n_inst, tb.tw, ws);
+  }
   return cudaGetLastError();
 }
 

@@ -135,3 +135,46 @@ def test_slot_regions_disjoint(logn):
         for u in range(N):
             a = xaddr(logn, slot * N + u)
             assert slot * region <= a < (slot + 1) * region
+
+
+def cswz(q, k):
+    """mul_ntt.cu cswz<Q>: XOR the 16-byte chunk index inside each 32-word row
+    with the row number's low bits."""
+    return k ^ (((k >> 5) & (q // 4 - 1)) << 2)
+
+
+def _wavefronts_128(addrs):
+    """Shared-memory wavefronts of one quarter-warp's 128-bit accesses: the
+    number of distinct 16-byte chunks that fall in the same bank group."""
+    groups = {}
+    for a in addrs:
+        groups.setdefault((a // 4) % 8, set()).add(a // 4)
+    return max(len(v) for v in groups.values())
+
+
+@pytest.mark.parametrize("q", [8, 16])
+@pytest.mark.parametrize("logm", range(5, 14))
+def test_epilogue_swizzle_conflict_free(q, logm):
+    """cswz<Q> is a bijection on [0, M) that keeps 16-byte chunks whole; a
+    warp's pass-layout writes (32 consecutive words, or two aligned 16-word
+    halves) stay conflict free; every quarter-warp's Q-words-per-thread
+    128-bit access (owners t .. t+7, also shifted by one owner as the H
+    publish is) hits 8 distinct bank groups — where plain row-major needs
+    Q/4 wavefronts."""
+    M = 1 << logm
+    perm = [cswz(q, k) for k in range(M)]
+    assert sorted(perm) == list(range(M))
+    assert all(cswz(q, k) // 4 == cswz(q, k - k % 4) // 4 and cswz(q, k) % 4 == k % 4 for k in range(M))
+    # pass-layout writes: aligned runs of 16 consecutive words map onto one aligned 16-word group
+    for k0 in range(0, M, 16):
+        banks = {cswz(q, k) % 32 for k in range(k0, k0 + 16)}
+        assert len(banks) == 16 and len({b // 16 for b in banks}) == 1
+    owners = M // q
+    for shift in (0, 1):
+        for t0 in range(0, owners - 8 - shift + 1, 8):
+            for c in range(q // 4):
+                addrs = [cswz(q, (t + shift) * q + 4 * c) for t in range(t0, t0 + 8)]
+                assert _wavefronts_128(addrs) == 1
+                plain = [(t + shift) * q + 4 * c for t in range(t0, t0 + 8)]
+                if owners >= 8:
+                    assert _wavefronts_128(plain) == q // 4

@@ -13,6 +13,8 @@ ballot-add formulation used in csrc/bn_scan.cuh against sequential folds:
   segmented scan leaks the previous segment's carry.
 """
 import itertools
+
+import pytest
 import random
 
 
@@ -177,3 +179,77 @@ def test_model_add_matches_python_int():
             B = sum(v << (32 * i) for i, v in enumerate(ys))
             S = (A + B) % (1 << (32 * M))
             assert _model_add(xs, ys, L, TPI) == [(S >> (32 * i)) & 0xFFFFFFFF for i in range(M)]
+
+
+def _chunk_sum(x, y, cin, L):
+    """bn_common.cuh chunk_sum on one L-limb chunk with carry-in cin: (s, g, p)."""
+    mask = (1 << (32 * L)) - 1
+    t = x + y + cin
+    s = t & mask
+    return s, t >> (32 * L), int(s == mask)
+
+
+def _scan_exclusive(gs, ps):
+    """exclusive carry scan over chunks (carry_op of PAPER.md:177-215)."""
+    out, c = [], 0
+    for g, p in zip(gs, ps):
+        out.append(c)
+        c = g | (p & c)
+    return out
+
+
+def _six_add_carry_save(a, b, n_chunks, L):
+    """Model of add6_kernel with BN_ADD6_CS (bn_common.cuh add_pending): the
+    final increment of addition k rides in addition k+1's carry chain, with
+    the carry-out cleared when the pending chunk was all ones with carry-in 1."""
+    W = 32 * L
+    mask = (1 << W) - 1
+    ca = [(a >> (W * j)) & mask for j in range(n_chunks)]
+    cb = [(b >> (W * j)) & mask for j in range(n_chunks)]
+    s, g, p = zip(*[_chunk_sum(x, y, 0, L) for x, y in zip(ca, cb)])
+    s, p = list(s), list(p)
+    cin = _scan_exclusive(g, p)
+    for k in range(1, 6):
+        z = ca if k % 2 else cb
+        gs = []
+        for j in range(n_chunks):
+            ov = p[j] & cin[j]
+            s[j], gj, p[j] = _chunk_sum(s[j], z[j], cin[j], L)
+            gs.append(gj & (1 - ov))
+        cin = _scan_exclusive(gs, p)
+    r = [(s[j] + cin[j]) & mask for j in range(n_chunks)]
+    return sum(v << (W * j) for j, v in enumerate(r))
+
+
+@pytest.mark.parametrize("L,n_chunks", [(1, 8), (2, 5), (4, 3)])
+def test_six_add_carry_save_model(L, n_chunks):
+    """The carry-save 6-Add equals six sequential additions (4a + 3b mod 2^B,
+    reading R17) on random, all-ones and carry-run inputs — in particular the
+    double-count case (pending chunk all ones with carry-in 1)."""
+    import random
+    rng = random.Random(L * 100 + n_chunks)
+    B = 32 * L * n_chunks
+    mod = 1 << B
+    ones = mod - 1
+    cases = [(ones, ones), (ones, 1), (1, ones), (0, ones), (ones, 0), (ones >> 1, ones)]
+    for _ in range(3000):
+        kind = rng.randrange(4)
+        if kind == 0:
+            a, b = rng.getrandbits(B), rng.getrandbits(B)
+        elif kind == 1:  # long runs of ones with sparse holes
+            a = ones ^ (1 << rng.randrange(B)) if rng.random() < 0.7 else ones
+            b = rng.getrandbits(8) << rng.randrange(B - 8)
+        elif kind == 2:  # chunks that are all ones / zero
+            W = 32 * L
+            a = sum(rng.choice([0, (1 << W) - 1, rng.getrandbits(W)]) << (W * j) for j in range(n_chunks))
+            b = sum(rng.choice([0, 1, (1 << W) - 1]) << (W * j) for j in range(n_chunks))
+        else:  # b = ~a + small -> 3b + 4a lands near multiples of 2^W
+            a = rng.getrandbits(B)
+            b = (ones ^ a) + rng.randrange(3)
+        cases.append((a % mod, b % mod))
+    for a, b in cases:
+        want = a
+        want = (a + b) % mod
+        for k in range(1, 6):
+            want = (want + (a if k % 2 else b)) % mod
+        assert _six_add_carry_save(a, b, n_chunks, L) == want, (hex(a), hex(b))

@@ -38,12 +38,12 @@ def main():
                      k.endswith("avg.pct_of_peak_sustained_active")]
             for k, x in sorted(pipes, key=lambda kv: -float(kv[1] or 0))[:8]:
                 print("  pipe %-57s %s %%" % (k[len("sm__inst_executed_pipe_"):], x))
-            st = [(k, d[k]) for k in hdr if k.startswith("smsp__average_warp_latency_issue_stalled_") or
-                  (k.startswith("smsp__warp_issue_stalled_") and k.endswith("per_warp_active.pct"))]
+            st = [(k, d[k]) for k in hdr if k.startswith("smsp__average_warps_issue_stalled_") and
+                  k.endswith("_per_issue_active.ratio")]
             tot = [(k, float(x)) for k, x in st if x not in ("", "n/a")]
             for k, x in sorted(tot, key=lambda kv: -kv[1])[:10]:
-                print("  stall %-56s %.2f" % (k.replace("smsp__warp_issue_stalled_", "").replace("_per_warp_active.pct", ""), x))
-
+                print("  stall/issue %-50s %.2f" % (k.replace("smsp__average_warps_issue_stalled_", "")
+                                                     .replace("_per_issue_active.ratio", ""), x))
 
 if __name__ == "__main__":
     main()
