@@ -22,7 +22,8 @@
  * 2^19 and 2^20 bits, bn_mul_classical to 2^19, with one instance per
  * thread-block cluster of 2 / 4 CTAs (carries, NTT exchanges and the L/H
  * publish through distributed shared memory);
- * bn_mul_wide_ntt stops at 2^17.  Other sizes -> BN_ESIZE.
+ * the fused (6-Add, Poly) and wide products stop at 2^18.  Other sizes ->
+ * BN_ESIZE.
  *
  * POINTERS: a, b, out are DEVICE pointers on the current CUDA device, 16-byte
  * aligned.  out may equal a or b exactly (in-place); a partial overlap is
@@ -152,9 +153,9 @@ uint64_t bn_poly_workspace_bytes(int op, uint64_t n_inst, uint32_t n_limbs, uint
  * follow bn_add's rules.  Classical: the truncated kernel's partition for
  * the low half and the same convolution on mirrored operands for the high
  * half; bits in [1024, 262144].  NTT: the N = 2m point
- * transforms already produce every coefficient; bits in [1024, 131072]
- * (a 262144-bit input returns BN_ESIZE: its 3N residues do not fit one
- * CTA's shared memory next to the exchange planes). */
+ * transforms already produce every coefficient; bits in [1024, 262144]
+ * (at 262144 bits one 512-thread CTA per instance with a single exchange
+ * plane and an incremental, element-wise Garner). */
 bn_status bn_mul_wide_classical(void *out, const void *a, const void *b, uint64_t n_inst,
                                 uint32_t n_limbs, uint32_t limb_bits, bn_stream_t stream);
 bn_status bn_mul_wide_ntt(void *out, const void *a, const void *b, uint64_t n_inst,

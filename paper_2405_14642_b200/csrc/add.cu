@@ -43,21 +43,6 @@ namespace cg = cooperative_groups;
 #ifndef BN_ADD6_CS
 #define BN_ADD6_CS 1  // 6-Add: carry-save chaining of the six additions (add_pending)
 #endif
-#ifndef BN_ADD6_PF
-#define BN_ADD6_PF 0  // 6-Add from 32K bits: persistent, next instance prefetched (add6_pf_kernel)
-#endif
-#ifndef BN_ADD6_PF_L10
-#define BN_ADD6_PF_L10 8
-#endif
-#ifndef BN_ADD6_PF_L11
-#define BN_ADD6_PF_L11 8
-#endif
-#ifndef BN_ADD6_PF_L12
-#define BN_ADD6_PF_L12 16
-#endif
-#ifndef BN_ADD6_PF_L13
-#define BN_ADD6_PF_L13 16
-#endif
 
 namespace bn {
 
@@ -148,77 +133,6 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
   }
 }
 
-// 6-Add from 32K bits with the next instance's operands in flight: the
-// register-resident add6_kernel leaves HBM idle while its six dependent CTA
-// scans run (ncu r02 at 256K: long-scoreboard and barrier stalls lead, 0.65
-// of the copy bandwidth).  Here every CTA is persistent and each thread
-// cp.async-copies its own 2 x L limbs of the NEXT instance into a shared
-// buffer (cswz<L> layout: conflict free) right after it has read the current
-// ones, so the copy overlaps the six scans and the store.  A thread only
-// reads back what it copied itself: no CTA barrier guards the buffer (the
-// copy is issued after the registers read from it have been consumed).
-template <int LOGM, int L>
-__global__ void __launch_bounds__(AddCfg<LOGM, L, 32>::BLOCK)
-    add6_pf_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
-  using C = AddCfg<LOGM, L, 32>;
-  static_assert(C::IPB == 1, "one instance per CTA");
-  extern __shared__ __align__(16) uint32_t buf[];  // [a | b][M], cswz<L>
-  __shared__ uint32_t agg[2][C::BLOCK / 32];
-  const uint32_t lt = threadIdx.x;
-  const uint32_t k0 = lt * L;
-  auto stage = [&](uint64_t inst) {
-    const uint64_t off = inst * (uint64_t)C::M + k0;
-#pragma unroll
-    for (int v = 0; v < L / 4; v++) {
-      cp_async16(buf + cswz<L>(k0 + 4 * v), a + off + 4 * v, true);
-      cp_async16(buf + C::M + cswz<L>(k0 + 4 * v), b + off + 4 * v, true);
-    }
-    cp_async_commit();
-  };
-  uint64_t inst = blockIdx.x;
-  if (inst < n_inst) stage(inst);
-  for (; inst < n_inst; inst += gridDim.x) {
-    uint32_t x[L], y[L], r[L];
-    cp_async_wait<0>();
-#pragma unroll
-    for (int v = 0; v < L / 4; v++) {
-      const uint4 xa = *reinterpret_cast<const uint4*>(buf + cswz<L>(k0 + 4 * v));
-      const uint4 xb = *reinterpret_cast<const uint4*>(buf + C::M + cswz<L>(k0 + 4 * v));
-      x[4 * v] = xa.x; x[4 * v + 1] = xa.y; x[4 * v + 2] = xa.z; x[4 * v + 3] = xa.w;
-      y[4 * v] = xb.x; y[4 * v + 1] = xb.y; y[4 * v + 2] = xb.z; y[4 * v + 3] = xb.w;
-    }
-    uint32_t g, p;
-    chunk_sum<L>(x, y, r, g, p);  // consumes the buffer's values
-    const uint64_t nxt = inst + gridDim.x;
-    if (nxt < n_inst) stage(nxt);
-    uint32_t cin = carry_scan<C::TPI>(g, p, agg[0]);  // a + b
-    add_pending<L, C::TPI>(r, x, cin, p, true, agg[1]);  // + a
-    add_pending<L, C::TPI>(r, y, cin, p, true, agg[0]);  // + b
-    add_pending<L, C::TPI>(r, x, cin, p, true, agg[1]);  // + a
-    add_pending<L, C::TPI>(r, y, cin, p, true, agg[0]);  // + b
-    add_pending<L, C::TPI>(r, x, cin, p, true, agg[1]);  // + a
-    chunk_apply<L>(x, r, cin);
-    store_limbs<L>(out + inst * (uint64_t)C::M + k0, r);
-    if constexpr (C::TPI > 32) __syncthreads();  // agg[0] reused by the next instance's first scan
-  }
-}
-
-template <int LOGM, int L>
-static cudaError_t launch_add6_pf_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
-                                    cudaStream_t st, int n_sm) {
-  using C = AddCfg<LOGM, L, 32>;
-  constexpr size_t smem = 2 * (size_t)C::M * sizeof(uint32_t);
-  static LaunchCache cache;
-  int per_sm = 0;
-  cudaError_t e = resident_ctas(cache, add6_pf_kernel<LOGM, L>, C::BLOCK, smem, &per_sm);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t cap = (uint64_t)n_sm * per_sm;
-  const unsigned grid = cap_grid((unsigned)(n_inst < cap ? n_inst : cap));
-  add6_pf_kernel<LOGM, L><<<grid, C::BLOCK, smem, st>>>(out, a, b, n_inst);
-  return cudaGetLastError();
-}
-
 // Sizes beyond one CTA (2^19, 2^20 bits): one instance per
 // thread-block cluster of CR = M / (1024 L) CTAs, CTA rank r holding
 // limbs [r M/CR, (r+1) M/CR), 1024 threads x L limbs.  The carry scan runs
@@ -244,6 +158,10 @@ __global__ void __launch_bounds__(1024, MB)
   const unsigned rank = cl.block_rank();
   const uint64_t n_cl = gridDim.x / CR;
   const uint32_t lo = threadIdx.x * L;
+  // every CTA of the cluster must be running before any CTA writes into its
+  // shared memory (the first cluster_carry_scan stores into the other CTAs'
+  // cta_agg before its own cluster barrier; compute-sanitizer racecheck r02)
+  cl.sync();
   auto stage = [&](uint64_t inst, int st) {
     const uint64_t off = inst * (uint64_t)M + (uint64_t)rank * SL + lo;
     uint32_t* s = sm + st * 2 * SL;
@@ -391,15 +309,6 @@ cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_
 
 cudaError_t launch_add6(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                         cudaStream_t st, int n_sm) {
-#if BN_ADD6_PF
-  switch (logm) {
-    case 10: return launch_add6_pf_t<10, BN_ADD6_PF_L10>(out, a, b, n_inst, st, n_sm);
-    case 11: return launch_add6_pf_t<11, BN_ADD6_PF_L11>(out, a, b, n_inst, st, n_sm);
-    case 12: return launch_add6_pf_t<12, BN_ADD6_PF_L12>(out, a, b, n_inst, st, n_sm);
-    case 13: return launch_add6_pf_t<13, BN_ADD6_PF_L13>(out, a, b, n_inst, st, n_sm);
-    default: break;
-  }
-#endif
   switch (logm) {
     case 5: return launch_add6_t<5>(out, a, b, n_inst, st, n_sm);
     case 6: return launch_add6_t<6>(out, a, b, n_inst, st, n_sm);

@@ -26,14 +26,14 @@ constexpr uint32_t kMinBits = 1024, kMaxBits = 1048576;
 
 // Largest log2(bits) per operation: 2^18 fits one CTA (the paper's range);
 // add and the NTT product go to 2^20, the classical product to 2^19, on
-// thread-block clusters; the wide NTT product stops at
-// 2^17 (shared memory).
+// thread-block clusters; the fused and wide products stop
+// at 2^18.
 int op_max_lb(int op) {
   switch (op) {
     case BN_OP_ADD: case BN_OP_MUL_NTT: return 20;
     case BN_OP_MUL_CLASSICAL: return 19;
-    case BN_OP_MUL_WIDE_NTT: return 17;
-    case BN_OP_ADD6: case BN_OP_POLY_CLASSICAL: case BN_OP_POLY_NTT: case BN_OP_MUL_WIDE_CLASSICAL: return 18;
+    case BN_OP_ADD6: case BN_OP_POLY_CLASSICAL: case BN_OP_POLY_NTT: case BN_OP_MUL_WIDE_CLASSICAL:
+    case BN_OP_MUL_WIDE_NTT: return 18;
     default: return -1;
   }
 }

@@ -268,7 +268,9 @@ BN_DEV void st_cluster(uint32_t caddr, uint32_t v) {
 // the warp-level ballot-add as its initial carry.  cta_agg: CR words of
 // shared memory per buffer, double-buffered by `parity` so consecutive
 // instances need one cluster barrier each.  Every thread of every CTA of the
-// cluster must call it.
+// cluster must call it, and the caller must have passed one cluster barrier
+// since the kernel started before the first call (the remote stores below
+// may only target CTAs that are already running).
 template <int CR, class Cluster>
 BN_DEV uint32_t cluster_carry_scan(uint32_t g, uint32_t p, uint32_t* agg, uint32_t* cta_agg, int parity,
                                    Cluster& cl) {

@@ -73,6 +73,14 @@ constexpr int kPolyNttTT = BN_POLY_NTT_TT;
 #ifndef BN_NTT_R32_PREFETCH_MAXLOG
 #define BN_NTT_R32_PREFETCH_MAXLOG 13
 #endif
+// Timing-only experiment (never in a shipped build): BN_DBG_TWCONST replaces
+// every twiddle load by a value derived from the pointer (no memory access),
+// to measure what the table loads cost.  Results are WRONG with it.
+#ifdef BN_DBG_TWCONST
+#define BN_DBG_TW(ptr) make_uint2((uint32_t)(uintptr_t)(ptr) & 0x3FFFFFFu, 0x5u)
+#else
+#define BN_DBG_TW(ptr) __ldg(ptr)
+#endif
 #ifndef BN_NTT_CL_MINB
 #define BN_NTT_CL_MINB 2
 #endif
@@ -199,7 +207,7 @@ BN_DEV void fwd_pass(uint32_t (&x)[NV][R], int t, const uint2* __restrict__ tw, 
         }
         continue;
       }
-      const uint2 w = __ldg(Ts + (el << PS::LO));
+      const uint2 w = BN_DBG_TW(Ts + (el << PS::LO));
 #pragma unroll
       for (int v = 0; v < NV; v++) {
         if (PADDED && P == 0 && s == 0) {
@@ -231,7 +239,7 @@ BN_DEV void inv_pass(uint32_t (&x)[R], int t, const uint2* __restrict__ tw, uint
         x[e | (1 << b)] = u - v + p2;
         continue;
       }
-      const uint2 w = __ldg(Ts + (el << PS::LO));
+      const uint2 w = BN_DBG_TW(Ts + (el << PS::LO));
       ct_bfly(x[e], x[e | (1 << b)], w, p, p2);
     }
   }
@@ -848,7 +856,12 @@ template <int LOGN>
 static cudaError_t launch_ntt_r32_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                     const NttTables& tb, cudaStream_t st, int n_sm) {
   using C = NttR32Cfg<LOGN>;
+#ifdef BN_DBG_R32_SMEM_KB  // timing experiment: pad the shared memory request (residency)
+  constexpr size_t need = C::SMEM_WORDS * sizeof(uint32_t);
+  constexpr size_t smem = need > (size_t)BN_DBG_R32_SMEM_KB * 1024 ? need : (size_t)BN_DBG_R32_SMEM_KB * 1024;
+#else
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
+#endif
   static LaunchCache cache;
   int per_sm = 0;
   cudaError_t e = resident_ctas(cache, mul_ntt_r32_kernel<LOGN>, C::T, smem, &per_sm);
@@ -1524,10 +1537,163 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T, NttWideCfg<LOGN>::MINB)
   }
 }
 
+// Wide product at 2^18 bits (N = 2^14 points, 2^15-limb result) in ONE CTA
+// of 512 threads x 32 register elements: the 16-element wide kernel keeps
+// 3 N raw residues (192 KiB) beside two exchange planes, which does not fit.
+// Here the forward transforms of a and b go one after the other through a
+// single plane (A-hat held in registers meanwhile) and Garner runs
+// incrementally, element by element in the pass-0 layout, so each thread only
+// ever touches its own coefficients until the aggregation:
+//   prime 0: R0[k] = r0;  prime 1: T1[k] = t1(y1, r0);
+//   prime 2: c = r0 + p0 t1 + p0 p1 t2 -> C0[k] | C1[k] | C2[k] (3 words)
+// in the three N-word regions (plane, R0, T1), then thread t aggregates the
+// 32 consecutive coefficients [32 t, 32 t + 32), publishes L / H (reading R8
+// with M -> 2M) and resolves all N = 2m limbs: 3 N words = 192 KiB.
+// The c regions use the 32-word-per-thread swizzle (chunk ^ row & 7): the
+// pass-layout writes and the 32-consecutive reads are both conflict free.
+BN_DEV int cswz32(int k) { return k ^ (((k >> 5) & 7) << 2); }
+
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 32, 1)
+    mul_wide_ntt_r32_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                            const uint2* __restrict__ tw) {
+  constexpr int N = 1 << LOGN, M = N / 2, T = N / 32;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* P0 = sm;          // exchange plane, later C0 / L
+  uint32_t* R0 = sm + N;      // r0, later C1 / H
+  uint32_t* T1 = sm + 2 * N;  // t1, later C2
+  uint32_t* agg = sm + 3 * N;
+  const int t = threadIdx.x;
+  const CrtConst& k = c_crt[LOGN];
+  const uint32_t q0 = c_pc[0].p, q1 = c_pc[1].p, q2 = c_pc[2].p;
+  for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x) {
+    const uint32_t* ai = a + inst * M;
+    const uint32_t* bi = b + inst * M;
+#pragma unroll 1
+    for (int j = 0; j < kNumPrimes; j++) {
+      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+      const uint2* twf = tw + (2 * j + 0) * (N - 1);
+      const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      uint32_t xa[1][32], xb[1][32];
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        xa[0][e] = red2(red2(__ldg(ai + t + e * (N / 32)), p2), p2);
+        xb[0][e] = red2(red2(__ldg(bi + t + e * (N / 32)), p2), p2);
+      }
+#pragma unroll
+      for (int e = 16; e < 32; e++) xa[0][e] = xb[0][e] = 0u;
+      r32_fwd1<LOGN>(xa, P0, t, twf, p, p2);
+      r32_fwd1<LOGN>(xb, P0, t, twf, p, p2);
+#pragma unroll
+      for (int e = 0; e < 32; e++) xa[0][e] = mont(xa[0][e], xb[0][e], p, pinv);
+      r32_inv<LOGN>(xa, P0, t, twi, p, p2);
+      // incremental Garner on this thread's own coefficients k = t + e N/32
+      if (j == 0) {
+#pragma unroll
+        for (int e = 0; e < 32; e++) R0[t + e * (N / 32)] = red2(shoup(xa[0][e], k.k0, k.k0_sh, q0), q0);
+      } else if (j == 1) {
+#pragma unroll
+        for (int e = 0; e < 32; e++) {
+          const uint32_t r0 = R0[t + e * (N / 32)];
+          const uint32_t u = shoup(xa[0][e], k.k1i, k.k1i_sh, q1);
+          const uint32_t v = shoup(r0, k.i01, k.i01_sh, q1);
+          T1[t + e * (N / 32)] = red2(red2(u + 2 * q1 - v, 2 * q1), q1);
+        }
+      } else {
+        __syncthreads();  // every read of the plane by the last inverse exchange is done
+#pragma unroll
+        for (int e = 0; e < 32; e++) {
+          const int kk = t + e * (N / 32);
+          const uint32_t r0 = R0[kk], t1 = T1[kk];
+          const uint32_t a2v = shoup(xa[0][e], k.k2i, k.k2i_sh, q2);
+          const uint32_t b2v = shoup(r0, k.i012, k.i012_sh, q2);
+          const uint32_t c2v = shoup(t1, k.p0i012, k.p0i012_sh, q2);
+          const uint32_t d = red2(b2v + c2v, 2 * q2);
+          const uint32_t t2 = red2(red2(a2v + 2 * q2 - d, 2 * q2), q2);
+          const uint64_t v64 = (uint64_t)q0 * t1 + r0;
+          const uint64_t w = (uint64_t)k.p01_lo * t2 + v64;
+          const uint64_t hh = (uint64_t)k.p01_hi * t2 + (w >> 32);
+          const int ks = cswz32(kk);
+          P0[ks] = (uint32_t)w;
+          R0[ks] = (uint32_t)hh;
+          T1[ks] = (uint32_t)(hh >> 32);
+        }
+      }
+    }
+    __syncthreads();
+    // aggregate the 32 consecutive coefficients [32 t, 32 t + 32)
+    uint32_t lows[32], h0, h1;
+    {
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const int ks = cswz32(32 * t + 4 * c);
+        const uint4 w0 = *reinterpret_cast<const uint4*>(P0 + ks);
+        const uint4 w1 = *reinterpret_cast<const uint4*>(R0 + ks);
+        const uint4 w2 = *reinterpret_cast<const uint4*>(T1 + ks);
+        const uint32_t c0[4] = {w0.x, w0.y, w0.z, w0.w}, c1[4] = {w1.x, w1.y, w1.z, w1.w},
+                       c2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          add3(a0, a1, a2, c0[q], c1[q], c2[q]);
+          lows[4 * c + q] = a0;
+          a0 = a1;
+          a1 = a2;
+          a2 = 0;
+        }
+      }
+      h0 = a0;
+      h1 = a1;
+    }
+    __syncthreads();  // every read of C0..C2 is done
+    // publish: L = P0 region, H = R0 region (N words each, cswz32 layout)
+    {
+#pragma unroll
+      for (int c = 0; c < 8; c++)
+        *reinterpret_cast<uint4*>(P0 + cswz32(32 * t + 4 * c)) =
+            make_uint4(lows[4 * c], lows[4 * c + 1], lows[4 * c + 2], lows[4 * c + 3]);
+      const int hb = t + 1 < T ? 32 * t + 32 : 0;  // the top chunk zeroes H[0, 32) (positions >= N dropped)
+      const uint32_t g0 = t + 1 < T ? h0 : 0u, g1 = t + 1 < T ? h1 : 0u;
+#pragma unroll
+      for (int c = 0; c < 8; c++)
+        *reinterpret_cast<uint4*>(R0 + cswz32(hb + 4 * c)) =
+            make_uint4(c == 0 ? g0 : 0u, c == 0 ? g1 : 0u, 0u, 0u);
+    }
+    __syncthreads();
+    // resolve R = L + H over the N = 2m limbs, 32 per thread
+    {
+      uint32_t x[32], y[32];
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const int ks = cswz32(32 * t + 4 * c);
+        const uint4 l = *reinterpret_cast<const uint4*>(P0 + ks);
+        const uint4 h = *reinterpret_cast<const uint4*>(R0 + ks);
+        x[4 * c] = l.x; x[4 * c + 1] = l.y; x[4 * c + 2] = l.z; x[4 * c + 3] = l.w;
+        y[4 * c] = h.x; y[4 * c + 1] = h.y; y[4 * c + 2] = h.z; y[4 * c + 3] = h.w;
+      }
+      add_regs_inplace<32, T>(x, y, true, agg);
+      store_limbs<32>(out + inst * N + 32 * t, x);
+    }
+    __syncthreads();  // regions / agg reused by the next instance
+  }
+}
+
 template <int LOGN>
 static cudaError_t launch_wide_ntt_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                      const NttTables& tb, cudaStream_t st, int n_sm) {
-  if constexpr (LOGN > 13) {
+  if constexpr (LOGN == 14) {
+    constexpr int T = (1 << LOGN) / 32;
+    constexpr size_t smem = (3 * (1 << LOGN) + T / 32) * sizeof(uint32_t);
+    static LaunchCache cache;
+    int per_sm = 0;
+    cudaError_t e = resident_ctas(cache, mul_wide_ntt_r32_kernel<LOGN>, T, smem, &per_sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t cap = (uint64_t)n_sm * per_sm;
+    const unsigned grid = cap_grid((unsigned)(n_inst < cap ? n_inst : cap));
+    mul_wide_ntt_r32_kernel<LOGN><<<grid, T, smem, st>>>(out, a, b, n_inst, tb.tw);
+    return cudaGetLastError();
+  } else if constexpr (LOGN > 13) {
     return cudaErrorInvalidValue;
   } else {
     using C = NttCfg<LOGN>;

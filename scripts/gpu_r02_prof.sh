@@ -17,7 +17,10 @@ prof() {  # tag op bits kernel_regex
   gzip -f gpurun_out/src_$1.csv
   [ "${KEEP_REP:-0}" = 1 ] || rm -f gpurun_out/prof_$1.ncu-rep
 }
-for spec in ${PROF_SPECS:-"ntt_4k mul_ntt 4096 ^mul_ntt_kernel" "ntt_128k mul_ntt 131072 ^mul_ntt_r32" "ntt_256k mul_ntt 262144 ^mul_ntt_r32" "add6_256k add6 262144 ^add6" "polyntt_4k poly_ntt 4096 ^poly_ntt"}; do
+# PROF_SPECS: ';'-separated "tag op bits kernel_regex" entries
+SPECS=${PROF_SPECS:-"ntt_4k mul_ntt 4096 ^mul_ntt_kernel;ntt_128k mul_ntt 131072 ^mul_ntt_r32;ntt_256k mul_ntt 262144 ^mul_ntt_r32;add6_256k add6 262144 ^add6;polyntt_4k poly_ntt 4096 ^poly_ntt"}
+IFS=';' read -ra SPEC_LIST <<< "$SPECS"
+for spec in "${SPEC_LIST[@]}"; do
   prof $spec
 done
 du -sh gpurun_out; ls gpurun_out

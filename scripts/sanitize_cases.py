@@ -1,7 +1,7 @@
 """Small invocations of every kernel for compute-sanitizer (memcheck /
-racecheck / synccheck / initcheck): each op at a small and a large size,
-ragged batches, a grid cap so the persistent paths run, and the cluster
-sizes.  Results are checked against the oracle (any mismatch exits 1)."""
+racecheck / synccheck / initcheck): every op at small and large sizes up to
+its maximum (fused and wide products to 256K bits), ragged batches, a grid
+cap so the persistent paths run, and (--big) the cluster sizes 512K / 1M.  Results are checked against the oracle (any mismatch exits 1)."""
 import os
 import sys
 
@@ -27,14 +27,14 @@ for cap in (0, 2):
         da, db = a.to(dev), b.to(dev)
         want = {"add": O.add(an, bnp), "mul": O.mul(an, bnp, nthreads=8)}
         ops = [("add", bn.add), ("mul", bn.mul_ntt)]
+        if bits <= bn.max_bits("mul_classical"):
+            ops += [("mul", bn.mul_classical)]
         if bits <= 262144:
             want["add6"] = O.add6(an, bnp)
-            ops += [("mul", bn.mul_classical), ("add6", bn.add6)]
-            if bits <= 65536:
-                want["poly"] = O.poly(an, bnp, nthreads=8)
-                want["wide"] = O.mul_full_rows(an, bnp)
-                ops += [("poly", bn.poly_classical), ("poly", bn.poly_ntt), ("wide", bn.mul_wide_classical),
-                        ("wide", bn.mul_wide_ntt)]
+            want["poly"] = O.poly(an, bnp, nthreads=8)
+            want["wide"] = O.mul_full_rows(an, bnp)
+            ops += [("add6", bn.add6), ("poly", bn.poly_classical), ("poly", bn.poly_ntt),
+                    ("wide", bn.mul_wide_classical), ("wide", bn.mul_wide_ntt)]
         for key, f in ops:
             got = inputs.to_numpy_u32(f(da, db))
             torch.cuda.synchronize()

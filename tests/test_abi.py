@@ -97,7 +97,7 @@ def test_u64_size_rules(lib):
 def test_introspection(lib):
     assert lib.bn_max_bits() == 1 << 20 and lib.bn_min_bits() == 1024
     assert [lib.bn_op_max_bits(op) for op in range(8)] == \
-        [1 << 20, 1 << 19, 1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 18, 1 << 17]
+        [1 << 20, 1 << 19, 1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 18, 1 << 18]
     assert lib.bn_status_string(3).startswith(b"BN_EALIGN")
     for op in range(6):
         assert lib.bn_launches_per_call(op, 4096) == 1
@@ -156,9 +156,9 @@ def test_wide_validation_before_launch(lib, op):
     assert _call(lib, op, O + 4, A, B, 4, 32, 32) == 3
     assert _call(lib, op, A, A, B, 4, 32, 32) == 4          # out == a: twice the size, overlaps
     assert _call(lib, op, A - 16, A, B, 4, 32, 32) == 4
-    if op == "bn_mul_wide_ntt":
-        assert _call(lib, op, O, A, B, 4, 8192, 32) == 2    # 256K-bit inputs: NTT wide unsupported
-    assert lib.bn_launches_per_call(7, 262144) == 0 and lib.bn_launches_per_call(6, 262144) == 1
+    assert _call(lib, op, O, A, B, 4, 16384, 32) == 2       # 512K-bit inputs: wide products stop at 2^18
+    assert lib.bn_launches_per_call(7, 262144) == 1 and lib.bn_launches_per_call(6, 262144) == 1
+    assert lib.bn_launches_per_call(7, 524288) == 0
 
 
 def test_build_stamp_tracks_flags():

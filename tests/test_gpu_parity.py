@@ -387,13 +387,9 @@ def test_parity_wide(bits, cls):
     got = inputs.to_numpy_u32(bn.mul_wide_classical(da, db))
     bad = _first_bad(got, want)
     assert bad is None, "wide classical %d bits %s: %s" % (bits, cls, bad)
-    if bits <= 131072:
-        got = inputs.to_numpy_u32(bn.mul_wide_ntt(da, db))
-        bad = _first_bad(got, want)
-        assert bad is None, "wide ntt %d bits %s: %s" % (bits, cls, bad)
-    else:
-        with pytest.raises(bn.BnError):
-            bn.mul_wide_ntt(da, db)
+    got = inputs.to_numpy_u32(bn.mul_wide_ntt(da, db))
+    bad = _first_bad(got, want)
+    assert bad is None, "wide ntt %d bits %s: %s" % (bits, cls, bad)
 
 
 @pytest.mark.parametrize("cap", [1, 4])
@@ -555,3 +551,28 @@ def test_in_place_fused(bits):
         da = a.to(DEV)
         f(da, da, out=da)
         assert np.array_equal(inputs.to_numpy_u32(da), ref(an, an)), name + " a=b=out"
+
+
+@pytest.mark.parametrize("cap", [1, 3])
+def test_wide_ntt_256k_grid_cap(cap):
+    """The 256K wide NTT kernel (one 512-thread CTA per instance, incremental
+    Garner) with CTAs that run several instances (grid cap): bit-exact vs the
+    oracle's full product and the classical wide kernel."""
+    bits = 262144
+    m = bits // 32
+    a, b = inputs.make_operands(5, m, seed=40 + cap, cls="MIX")
+    want = O.mul_full_rows(inputs.to_numpy_u32(a), inputs.to_numpy_u32(b))
+    da, db = a.to(DEV), b.to(DEV)
+    bn.debug_set_grid_cap(cap)
+    try:
+        got = inputs.to_numpy_u32(bn.mul_wide_ntt(da, db))
+    finally:
+        bn.debug_set_grid_cap(0)
+    assert _first_bad(got, want) is None
+    ones, _ = inputs.make_operands(3, m, seed=1, cls="ONES", device=DEV)
+    w = bn.mul_wide_ntt(ones, ones)  # (2^B - 1)^2 = 2^2B - 2^(B+1) + 1
+    exp = torch.zeros((2 * m,), dtype=torch.int32, device=DEV)
+    exp[0] = 1
+    exp[m] = -2
+    exp[m + 1:] = -1
+    assert torch.equal(w, exp.expand(3, 2 * m))
