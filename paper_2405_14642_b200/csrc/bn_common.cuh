@@ -22,6 +22,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "bn_config.h"
+
 #define BN_DEV __device__ __forceinline__
 
 namespace bn {

@@ -1,0 +1,134 @@
+// bn_config.h — the shipped kernel geometry, one table.
+//
+// Every tunable of the three kernel families lives here with the value the
+// library ships and the A/B evidence behind it (ms per paper batch,
+// NumBits * NumInsts = 2^32, one B200, scripts/ab.sh unless noted).  A
+// variant build overrides a value on the nvcc command line
+// (`python -m paper_2405_14642_b200._build --variant NAME -DBN_X=...`), which
+// writes ab/libbn_NAME.so and never the in-tree libbn.so (_build.py): the
+// defaults below ARE the shipped configuration.  DESIGN.md §6b explains the
+// per-size choices.
+//
+// | knob                        | shipped | meaning / evidence                                           |
+// |-----------------------------|---------|--------------------------------------------------------------|
+// | add                         |         |                                                              |
+// | BN_ADD_BIG                  | 2       | 2^19 / 2^20 bits: 0 = 1024-thread clusters, cp.async staging, |
+// |                             |         | 1 CTA/SM (0.402 / 0.490); 1 = one CTA x 16 limbs (512K), a    |
+// |                             |         | 2-CTA cluster x 16 limbs (1M) (0.331 / 0.379); 2 = 2 / 4-CTA  |
+// |                             |         | clusters, 8 limbs, direct loads, 2 clusters/SM (0.310/0.336) |
+// | BN_ADD_CL_STAGES            | 2       | cp.async stages of variant 0 (3 measured no faster)          |
+// | BN_ADD6_BMIN_MID            | 128     | 6-Add CTA size floor from 32K bits (32K 0.324 -> 0.286)      |
+// | BN_ADD6_L12, BN_ADD6_L13    | 16, 16  | 6-Add limbs/thread at 128K / 256K (L=8 at 256K: 1 CTA/SM,    |
+// |                             |         | 0.555 -> 0.377; L=32 at 128K 0.341 -> 0.474)                  |
+// | BN_ADD6_TMA_MIN             | 12      | log2 limbs from which 6-Add streams through the TMA ring      |
+// |                             |         | (add6_tma_kernel)                                            |
+// | classical                   |         |                                                              |
+// | BN_CLASSICAL_TT             | 0       | 0 = per-size CTA target (MulCCfg), else a fixed target       |
+// | BN_CLASSICAL_1K_TT          | 128     | CTA target of the column-group kernel at 1K (when T1 = 0)    |
+// | BN_CLASSICAL_2K_MINB        | 6       | residency target of the 2K column-group kernel               |
+// | BN_CLASSICAL_T1             | 1       | 1K 1-Mul / wide: one thread per instance (0.470 -> 0.347)    |
+// | BN_CLASSICAL_T1_2K          | 1       | 2K 1-Mul one thread per instance (0.746 -> 0.607)            |
+// | BN_CLASSICAL_T1_WIDE_2K     | 1       | 2K wide one thread per instance (1.754 -> 1.240)             |
+// | BN_CLASSICAL_T1_MINB        | 5       | 1K residency: 4 -> 0.395, 5 -> 0.389, 6 -> 0.398             |
+// | BN_CLASSICAL_T1_MINB_2K     | 6       | 2K residency: 4 -> 0.612, 6 -> 0.607 (168 registers)         |
+// | BN_POLY_T1_2K               | 1       | 2K Poly one thread per instance (2.685 -> 2.297)             |
+// | BN_POLY_T1_MINB             | 6       | 168 registers, 6 CTAs x 32 KiB per SM                        |
+// | NTT                         |         |                                                              |
+// | BN_NTT_TT                   | 64      | CTA target of the 16-element kernel, N <= 2^BN_NTT_TT_MAXLOG: |
+// |                             |         | 4K 256 -> 2.953, 128 -> 2.879, 64 -> 2.873, 32 -> 2.884       |
+// | BN_NTT_TT_MAXLOG            | 12      | larger N use 256-thread targets (16K -9.4%, 32K -7.7%)        |
+// | BN_NTT_SMALL_THREADS        | 768     | residency target for N <= 256: 768 -> 2.882 (80 regs),       |
+// |                             |         | 896 -> 2.891, 1024 -> 2.921                                   |
+// | BN_NTT_R32_MIN              | 13      | log2 N from which the 32-element kernel runs (128K: 6.45 ->  |
+// |                             |         | 6.23; 256K: 7.37 -> 6.52; it loses at 32K / 64K)              |
+// | BN_NTT_R32_PREFETCH_MAXLOG  | 13      | next prime's limbs prefetched during the inverse up to this  |
+// |                             |         | log2 N (128K 6.27 -> 6.17; 256K 6.53 -> 6.66, spills)         |
+// | BN_NTT_CL_T, BN_NTT_CL_MINB | 1024, 2 | threads / residency of the 16-element cluster kernel, built   |
+// |                             |         | only with -DBN_NTT_CL16 (the 32-element one ships: 2^19 9.55 |
+// |                             |         | -> 8.30, 2^20 12.1 -> 11.5)                                   |
+// | BN_POLY_NTT_TT              | 256     | CTA target of the 16-element Poly kernel (64: 1K 9.21 ->     |
+// |                             |         | 10.54, 4K 10.18 -> 11.65; 128: 4K 10.27 vs 9.91)              |
+// | BN_POLY_R32_MIN             | 13      | log2 N from which Poly runs on the 32-element layout (12:    |
+// |                             |         | 64K 15.94 -> 17.77)                                           |
+#pragma once
+
+// ---- add
+#ifndef BN_ADD_BIG
+#define BN_ADD_BIG 2
+#endif
+#ifndef BN_ADD_CL_STAGES
+#define BN_ADD_CL_STAGES 2
+#endif
+#ifndef BN_ADD6_BMIN_MID
+#define BN_ADD6_BMIN_MID 128
+#endif
+#ifndef BN_ADD6_L12
+#define BN_ADD6_L12 16
+#endif
+#ifndef BN_ADD6_L13
+#define BN_ADD6_L13 16
+#endif
+#ifndef BN_ADD6_TMA_MIN
+#define BN_ADD6_TMA_MIN 12
+#endif
+
+// ---- classical
+#ifndef BN_CLASSICAL_TT
+#define BN_CLASSICAL_TT 0
+#endif
+#ifndef BN_CLASSICAL_1K_TT
+#define BN_CLASSICAL_1K_TT 128
+#endif
+#ifndef BN_CLASSICAL_2K_MINB
+#define BN_CLASSICAL_2K_MINB 6
+#endif
+#ifndef BN_CLASSICAL_T1
+#define BN_CLASSICAL_T1 1
+#endif
+#ifndef BN_CLASSICAL_T1_2K
+#define BN_CLASSICAL_T1_2K 1
+#endif
+#ifndef BN_CLASSICAL_T1_WIDE_2K
+#define BN_CLASSICAL_T1_WIDE_2K 1
+#endif
+#ifndef BN_CLASSICAL_T1_MINB
+#define BN_CLASSICAL_T1_MINB 5
+#endif
+#ifndef BN_CLASSICAL_T1_MINB_2K
+#define BN_CLASSICAL_T1_MINB_2K 6
+#endif
+#ifndef BN_POLY_T1_2K
+#define BN_POLY_T1_2K 1
+#endif
+#ifndef BN_POLY_T1_MINB
+#define BN_POLY_T1_MINB 6
+#endif
+
+// ---- NTT
+#ifndef BN_NTT_TT
+#define BN_NTT_TT 64
+#endif
+#ifndef BN_NTT_TT_MAXLOG
+#define BN_NTT_TT_MAXLOG 12
+#endif
+#ifndef BN_NTT_SMALL_THREADS
+#define BN_NTT_SMALL_THREADS 768
+#endif
+#ifndef BN_NTT_R32_MIN
+#define BN_NTT_R32_MIN 13
+#endif
+#ifndef BN_NTT_R32_PREFETCH_MAXLOG
+#define BN_NTT_R32_PREFETCH_MAXLOG 13
+#endif
+#ifndef BN_NTT_CL_T
+#define BN_NTT_CL_T 1024
+#endif
+#ifndef BN_NTT_CL_MINB
+#define BN_NTT_CL_MINB 2
+#endif
+#ifndef BN_POLY_NTT_TT
+#define BN_POLY_NTT_TT 256
+#endif
+#ifndef BN_POLY_R32_MIN
+#define BN_POLY_R32_MIN 13
+#endif

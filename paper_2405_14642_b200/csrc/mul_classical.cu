@@ -31,15 +31,6 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef BN_CLASSICAL_1K_TT
-#define BN_CLASSICAL_1K_TT 128  // target CTA size at 1K bits
-#endif
-#ifndef BN_CLASSICAL_2K_MINB
-#define BN_CLASSICAL_2K_MINB 6  // residency target of the 2K-bit 1-Mul kernel
-#endif
-#ifndef BN_CLASSICAL_TT
-#define BN_CLASSICAL_TT 0  // 0: per-size default (MulCCfg); else a fixed target CTA size
-#endif
 
 namespace bn {
 
@@ -766,12 +757,6 @@ static cudaError_t launch_polyc_t(uint32_t* out, const uint32_t* a, const uint32
 template <int M, bool WIDE>
 static cudaError_t launch_mulc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                   cudaStream_t st, int n_sm);
-#ifndef BN_CLASSICAL_T1
-#define BN_CLASSICAL_T1 1  // 0: 1K bits use the column-group kernel
-#endif
-#ifndef BN_CLASSICAL_T1_WIDE_2K
-#define BN_CLASSICAL_T1_WIDE_2K 1  // wide 2K one thread per instance: 1.754 -> 1.240 ms by A/B
-#endif
 
 cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                       uint64_t n_inst, cudaStream_t st, int n_sm) {
@@ -793,9 +778,6 @@ cudaError_t poly_classical_geometry(int logm, uint64_t n_inst, int n_sm, uint64_
 template <int M>
 static cudaError_t launch_polyc_t1(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                    cudaStream_t st, int n_sm);
-#ifndef BN_POLY_T1_2K
-#define BN_POLY_T1_2K 1
-#endif
 
 cudaError_t launch_poly_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                   uint64_t n_inst, uint32_t* ws, uint64_t ws_words, cudaStream_t st,
@@ -952,15 +934,6 @@ constexpr int kT1Threads = 128;
 // 55% busy, long-scoreboard stalls 17 per issue: ncu).  16-byte chunk c of
 // row r sits at r * 8 + (c ^ (r & 7)): a quarter-warp reading chunk k of its
 // 8 rows touches 8 distinct bank quads.
-#ifndef BN_CLASSICAL_T1_MINB
-#define BN_CLASSICAL_T1_MINB 5  // A/B at 1K (ms): 4 -> 0.395, 5 -> 0.389, 6 -> 0.398
-#endif
-#ifndef BN_CLASSICAL_T1_MINB_2K
-#define BN_CLASSICAL_T1_MINB_2K 6  // A/B at 2K (ms): 4 -> 0.612, 6 -> 0.607 (168 registers)
-#endif
-#ifndef BN_CLASSICAL_T1_2K
-#define BN_CLASSICAL_T1_2K 1  // 2K bits one thread per instance: 0.746 -> 0.607 ms by A/B
-#endif
 // tiles in flight per warp (cp.async stages of A | B); A/B at 1K (ms):
 // 1-Mul 1 stage 0.348 / 2 stages 0.368, full product 0.697 / 0.635
 constexpr int t1_stages(int m, bool wide) { return m == 32 && wide ? 2 : 1; }
@@ -1142,9 +1115,6 @@ BN_DEV void t1_prod(const uint32_t (&x)[M], const uint32_t (&y)[M], Add add, Sin
 // 2K (M = 64): the operand tile alone is 16 KiB per warp, so a b and a a + b
 // overwrite it (each lane its own rows) and the next tile is loaded after
 // the product instead of during it (PF = false).
-#ifndef BN_POLY_T1_MINB
-#define BN_POLY_T1_MINB 6  // 168 registers, 6 CTAs x 32 KiB per SM
-#endif
 template <int M>
 __global__ void __launch_bounds__(kPolyT1Threads, BN_POLY_T1_MINB)
     poly_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {

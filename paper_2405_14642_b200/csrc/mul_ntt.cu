@@ -38,41 +38,17 @@ namespace cg = cooperative_groups;
 // 2^20: 13.3 vs 12.2), so the defaults are 1024 and one CTA up to 2^18.
 // -DBN_NTT14_CLUSTER -DBN_NTT_CL_T=512 [-DBN_NTT_CL_MINB=1] rebuild the variants.
 // target CTA size of the 16-element kernel for N <= 256 (several instances per CTA)
-#ifndef BN_NTT_TT
-#define BN_NTT_TT 64  // A/B at 4K: 256 -> 2.953 ms, 128 -> 2.879, 64 -> 2.873, 32 -> 2.884
-#endif
-#ifndef BN_NTT_TT_MAXLOG
-#define BN_NTT_TT_MAXLOG 12  // A/B: 16K -9.4%, 32K -7.7% vs 256-thread CTAs
-#endif
 // target CTA size of the 16-element Poly kernel
-#ifndef BN_POLY_NTT_TT
-#define BN_POLY_NTT_TT 256
-#endif
 constexpr int kPolyNttTT = BN_POLY_NTT_TT;
 // smallest log2 N whose Poly runs on the 32-element layout
-#ifndef BN_POLY_R32_MIN
-#define BN_POLY_R32_MIN 13
-#endif
 // Poly on the 32-element layout: forward-transform a and b one at a time
-#ifndef BN_POLY_R32_SEQ
-#define BN_POLY_R32_SEQ 0
-#endif
 // residency target (threads per SM) of the 16-element kernel for N <= 256.
 // A/B at 4K (ms): 768 -> 2.882 (80 registers), 896 -> 2.891 (72), 1024 ->
 // 2.921 (64; shared memory caps all three at 12-14 CTAs of 64 threads)
-#ifndef BN_NTT_SMALL_THREADS
-#define BN_NTT_SMALL_THREADS 768
-#endif
 // smallest log2 N that uses the 32-element-per-thread kernel
-#ifndef BN_NTT_R32_MIN
-#define BN_NTT_R32_MIN 13
-#endif
 // r32 kernel: prefetch the next prime's / instance's raw limbs during the
 // inverse for LOGN <= this (A/B on B200, ms per paper batch: 128K 6.27 ->
 // 6.17; 256K 6.53 -> 6.66, where the 32 extra live registers add spills)
-#ifndef BN_NTT_R32_PREFETCH_MAXLOG
-#define BN_NTT_R32_PREFETCH_MAXLOG 13
-#endif
 // Timing-only experiment (never in a shipped build): BN_DBG_TWCONST replaces
 // every twiddle load by a value derived from the pointer (no memory access),
 // to measure what the table loads cost.  Results are WRONG with it.
@@ -80,12 +56,6 @@ constexpr int kPolyNttTT = BN_POLY_NTT_TT;
 #define BN_DBG_TW(ptr) make_uint2((uint32_t)(uintptr_t)(ptr) & 0x3FFFFFFu, 0x5u)
 #else
 #define BN_DBG_TW(ptr) __ldg(ptr)
-#endif
-#ifndef BN_NTT_CL_MINB
-#define BN_NTT_CL_MINB 2
-#endif
-#ifndef BN_NTT_CL_T
-#define BN_NTT_CL_T 1024
 #endif
 
 
@@ -993,27 +963,6 @@ __global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
       const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
       const uint2* twf = tw + (2 * j + 0) * (N - 1);
       const uint2* twi = tw + (2 * j + 1) * (N - 1);
-#if BN_POLY_R32_SEQ
-      // A and B transformed one after the other through plane 0 (32 data
-      // registers instead of 64) and parked as soon as each is done
-      {
-        uint32_t xa[1][32];
-#pragma unroll
-        for (int e = 0; e < 16; e++) xa[0][e] = red2(red2(__ldg(ai + t + e * (N / 32)), p2), p2);
-#pragma unroll
-        for (int e = 16; e < 32; e++) xa[0][e] = 0u;
-        r32_fwd1<LOGN>(xa, X, t, twf, p, p2);
-#pragma unroll
-        for (int e = 0; e < 32; e++) Res[e * C::T + t] = xa[0][e];
-#pragma unroll
-        for (int e = 0; e < 16; e++) xa[0][e] = red2(red2(__ldg(bi + t + e * (N / 32)), p2), p2);
-#pragma unroll
-        for (int e = 16; e < 32; e++) xa[0][e] = 0u;
-        r32_fwd1<LOGN>(xa, X, t, twf, p, p2);
-#pragma unroll
-        for (int e = 0; e < 32; e++) X[N + e * C::T + t] = xa[0][e];
-      }
-#else
       uint32_t xab[2][32];
       r32_load<LOGN, false>(xab, ai, bi, t, p2);
       r32_fwd<LOGN>(xab, X, t, twf, p, p2);
@@ -1026,7 +975,6 @@ __global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
         Res[e * C::T + t] = xab[0][e];
         X[N + e * C::T + t] = xab[1][e];
       }
-#endif
 #pragma unroll 1
       for (int P = 0; P < 3; P++) {
         // P = 0: A-hat^2, 1: B-hat^2, 2: A-hat B-hat
