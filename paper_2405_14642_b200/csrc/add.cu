@@ -15,8 +15,6 @@
 // tail effects.  HBM-bound: 3 * bits / 8 algorithmic bytes per instance
 // (PAPER.md:929).
 #include <cooperative_groups.h>
-#include <cuda.h>
-#include <cudaTypedefs.h>
 
 #include "bn_common.cuh"
 #include "bn_kernels.h"
@@ -106,204 +104,6 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
     if (valid) store_limbs<L>(out + off, r);
     if constexpr (C::TPI > 32) __syncthreads();
   }
-}
-
-// ------------------------------------------------------------ 6-Add fed by TMA
-// From 32K bits (BN_ADD6_TMA_MIN) the register-resident add6_kernel exposes
-// its load latency: ncu r02 at 256K puts 35% of the stall samples in the
-// load + first-scan phase (long-scoreboard 55% of them), and registers (a, b
-// and r: 3 words per limb) cap the SM at two 256K instances, so HBM idles
-// while the six dependent CTA scans run (0.66 - 0.77 of the copy bandwidth at
-// 128K / 256K).  Here one persistent 512-thread CTA per SM streams its
-// instances through a 3-stage ring in shared memory: thread 0 issues two
-// tensor bulk copies per stage (cp.async.bulk.tensor.2d — the operands as a
-// [rows][32 words] tensor, 256 rows = 32 KiB per operand per stage, 128-byte
-// swizzle so the 16-limbs-per-thread reads are bank-conflict free) that
-// complete on the stage's mbarrier; the threads wait on it, run the six
-// carry-save additions with only r in registers (a and b are re-read from
-// the stage, four limbs at a time) and store r.  The last scan's CTA barrier
-// orders every read of a stage before thread 0 refills it, so two stages
-// (64 KiB each) are always in flight while one is consumed.
-constexpr int kA6Threads = 512;                 // per CTA
-constexpr int kA6Rows = kA6Threads * 16 / 32;   // 256 rows of 32 words per operand per stage
-constexpr int kA6StageBytes = 2 * kA6Rows * 128;  // a | b
-constexpr int kA6Stages = 3;
-
-BN_DEV uint32_t mbar_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-BN_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar_addr(bar)), "r"(count) : "memory");
-}
-BN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_addr(bar)), "r"(bytes)
-               : "memory");
-}
-BN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(mbar_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-BN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(mbar_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(mbar_addr(bar))
-      : "memory");
-}
-
-// 128-byte swizzle of the TMA box: 16-byte chunk c of row r sits at chunk
-// c ^ (r & 7) (the smem stage is 1024-byte aligned).
-BN_DEV const uint4* a6_chunk(const uint32_t* stage, int row, int c) {
-  return reinterpret_cast<const uint4*>(stage + row * 32 + 4 * (c ^ (row & 7)));
-}
-
-template <int L, bool BOTH>
-BN_DEV void chunk_sum_tma(uint32_t (&r)[L], const uint32_t* xs, const uint32_t* ys, int row, int c0,
-                          uint32_t cin, uint32_t& g, uint32_t& p) {
-  uint32_t c = cin, all = 0xFFFFFFFFu;
-#pragma unroll
-  for (int v = 0; v < L / 4; v++) {
-    const uint4 yv = *a6_chunk(ys, row, c0 + v);
-    uint32_t xv[4];
-    if constexpr (BOTH) {
-      const uint4 t = *a6_chunk(xs, row, c0 + v);
-      xv[0] = t.x; xv[1] = t.y; xv[2] = t.z; xv[3] = t.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; i++) xv[i] = r[4 * v + i];
-    }
-    const uint32_t yy[4] = {yv.x, yv.y, yv.z, yv.w};
-    uint32_t t[4];
-    c = add4_cc(t, xv, yy, c);
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      r[4 * v + i] = t[i];
-      all &= t[i];
-    }
-  }
-  g = c;
-  p = all == 0xFFFFFFFFu;
-}
-
-template <int LOGM>
-__global__ void __launch_bounds__(kA6Threads, 1)
-    add6_tma_kernel(uint32_t* out, const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b, uint64_t n_inst) {
-  constexpr int L = 16, M = 1 << LOGM, TPI = M / L, IPB = kA6Threads / TPI;
-  static_assert(TPI >= 64 && TPI <= kA6Threads, "32K .. 256K bits");
-  extern __shared__ uint8_t smem_raw[];
-  uint32_t* ring = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full[kA6Stages];
-  __shared__ uint32_t agg[2][kA6Threads / 32];
-  const int tid = threadIdx.x;
-  const int slot = tid / TPI, lt = tid % TPI;
-  const uint64_t n_items = (n_inst + IPB - 1) / IPB;
-  auto issue = [&](uint64_t item, int s) {
-    uint32_t* st = ring + s * (kA6StageBytes / 4);
-    mbar_expect_tx(&full[s], kA6StageBytes);
-    const int row0 = (int)(item * kA6Rows);  // rows of 32 words: item * IPB * M / 32
-    tma_load_2d(st, &map_a, 0, row0, &full[s]);
-    tma_load_2d(st + kA6Rows * 32, &map_b, 0, row0, &full[s]);
-  };
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < kA6Stages; s++) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < kA6Stages; s++) {
-      const uint64_t item = blockIdx.x + (uint64_t)s * gridDim.x;
-      if (item < n_items) issue(item, s);
-    }
-  }
-  // this thread's 16 limbs: row (slot M + 16 lt) / 32 of the stage, chunks c0 .. c0+3
-  const int row = (slot * M + lt * L) / 32;
-  const int c0 = ((lt * L) % 32) / 4;
-  int s = 0;
-  uint32_t phase = 0;
-  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const uint32_t* st = ring + s * (kA6StageBytes / 4);
-    const uint32_t* as = st;
-    const uint32_t* bs = st + kA6Rows * 32;
-    mbar_wait(&full[s], phase);
-    const uint64_t inst = item * IPB + slot;
-    const bool valid = inst < n_inst;
-    uint32_t r[L], g, p, cin;
-    chunk_sum_tma<L, true>(r, as, bs, row, c0, 0u, g, p);  // a + b
-    if (!valid) g = p = 0;
-    cin = carry_scan<TPI>(g, p, agg[0]);
-#pragma unroll
-    for (int k = 1; k < 6; k++) {  // + a, + b, + a, + b, + a  (carry-save, as add_pending)
-      const uint32_t ov = p & cin;
-      chunk_sum_tma<L, false>(r, nullptr, (k & 1) ? as : bs, row, c0, cin, g, p);
-      g &= ~ov;
-      if (!valid) g = p = 0;
-      cin = carry_scan<TPI>(g, p, agg[k & 1]);
-    }
-    // the last scan's CTA barrier: every thread is done reading this stage
-    if (tid == 0) {
-      const uint64_t nxt = item + (uint64_t)kA6Stages * gridDim.x;
-      if (nxt < n_items) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(nxt, s);
-      }
-    }
-    chunk_apply<L>(r, r, cin);
-    if (valid) store_limbs<L>(out + inst * (uint64_t)M + lt * L, r);
-    __syncthreads();  // agg[0] reused by the next item's first scan
-    if (++s == kA6Stages) {
-      s = 0;
-      phase ^= 1;
-    }
-  }
-}
-
-// host: a [rows][32 words] view of one operand (rows = n_inst * M / 32), box
-// 32 words x kA6Rows rows, 128-byte swizzle
-static cudaError_t a6_tensor_map(CUtensorMap* map, const uint32_t* base, uint64_t rows) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  const cuuint64_t dims[2] = {32, rows};
-  const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {32, (cuuint32_t)kA6Rows};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box,
-                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
-template <int LOGM>
-static cudaError_t launch_add6_tma_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
-                                     cudaStream_t st, int n_sm) {
-  constexpr int M = 1 << LOGM, IPB = kA6Threads / (M / 16);
-  constexpr size_t smem = (size_t)kA6Stages * kA6StageBytes + 1024;
-  const uint64_t rows = n_inst * (uint64_t)M / 32;
-  if (rows >= (1ull << 31)) return cudaErrorInvalidValue;  // TMA coordinates are int32
-  CUtensorMap ma, mb;
-  cudaError_t e = a6_tensor_map(&ma, a, rows);
-  if (e != cudaSuccess) return e;
-  e = a6_tensor_map(&mb, b, rows);
-  if (e != cudaSuccess) return e;
-  static LaunchCache cache;
-  int per_sm = 0;
-  e = resident_ctas(cache, add6_tma_kernel<LOGM>, kA6Threads, smem, &per_sm);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t n_items = (n_inst + IPB - 1) / IPB;
-  const uint64_t cap = (uint64_t)n_sm * per_sm;
-  const unsigned grid = cap_grid((unsigned)(n_items < cap ? n_items : cap));
-  add6_tma_kernel<LOGM><<<grid, kA6Threads, smem, st>>>(out, ma, mb, n_inst);
-  return cudaGetLastError();
 }
 
 // Sizes beyond one CTA (2^19, 2^20 bits): one instance per
@@ -482,15 +282,6 @@ cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_
 
 cudaError_t launch_add6(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                         cudaStream_t st, int n_sm) {
-  if (logm >= BN_ADD6_TMA_MIN) {
-    switch (logm) {
-      case 10: return launch_add6_tma_t<10>(out, a, b, n_inst, st, n_sm);
-      case 11: return launch_add6_tma_t<11>(out, a, b, n_inst, st, n_sm);
-      case 12: return launch_add6_tma_t<12>(out, a, b, n_inst, st, n_sm);
-      case 13: return launch_add6_tma_t<13>(out, a, b, n_inst, st, n_sm);
-      default: break;
-    }
-  }
   switch (logm) {
     case 5: return launch_add6_t<5>(out, a, b, n_inst, st, n_sm);
     case 6: return launch_add6_t<6>(out, a, b, n_inst, st, n_sm);

@@ -20,8 +20,6 @@
 // | BN_ADD6_BMIN_MID            | 128     | 6-Add CTA size floor from 32K bits (32K 0.324 -> 0.286)      |
 // | BN_ADD6_L12, BN_ADD6_L13    | 16, 16  | 6-Add limbs/thread at 128K / 256K (L=8 at 256K: 1 CTA/SM,    |
 // |                             |         | 0.555 -> 0.377; L=32 at 128K 0.341 -> 0.474)                  |
-// | BN_ADD6_TMA_MIN             | 12      | log2 limbs from which 6-Add streams through the TMA ring      |
-// |                             |         | (add6_tma_kernel)                                            |
 // | classical                   |         |                                                              |
 // | BN_CLASSICAL_TT             | 0       | 0 = per-size CTA target (MulCCfg), else a fixed target       |
 // | BN_CLASSICAL_1K_TT          | 128     | CTA target of the column-group kernel at 1K (when T1 = 0)    |
@@ -67,9 +65,6 @@
 #endif
 #ifndef BN_ADD6_L13
 #define BN_ADD6_L13 16
-#endif
-#ifndef BN_ADD6_TMA_MIN
-#define BN_ADD6_TMA_MIN 12
 #endif
 
 // ---- classical
