@@ -321,14 +321,15 @@ def stats(ts):
             "timed_ms": sum(ts)}
 
 
-def load_ncu(kernel: str, bits: int):
-    """Counters of the committed ncu --set full capture of `kernel` at `bits`
-    (profiles/ncu_kernels.json, key "<kernel>@<bits>"): DRAM bytes per
-    launch and FMA-heavy / ALU / issue-active percentages, else None."""
+def load_ncu(op: str, bits: int):
+    """Counters of the committed ncu --set full capture of `op`'s kernel at
+    `bits` (profiles/ncu_kernels.json, key "<op>@<bits>"): kernel name, DRAM
+    bytes per launch and FMA-heavy / ALU / issue-active percentages, else
+    None."""
     p = os.path.join(ROOT, "profiles", "ncu_kernels.json")
     try:
         with open(p) as f:
-            return json.load(f).get("%s@%d" % (kernel, bits))
+            return json.load(f).get("%s@%d" % (op, bits))
     except Exception:
         return None
 
@@ -385,6 +386,9 @@ def per_size(args, bn, inputs, torch, dev, stream, rk, peaks, shard):
                     r["Gu32ops/s"] = total * work(bits)["u32ops"] / sec / 1e9
                 r.update({k: v for k, v in fractions(name, bits, n, st["ms"], peaks).items()
                           if k != "GB/s"})
+                nc = load_ncu(name, bits)
+                if nc:  # pipe fractions of the committed ncu capture
+                    r["ncu"] = {k: nc[k] for k in ("fmaheavy_pct", "alu_pct", "issue_pct", "dram_bytes") if k in nc}
                 row[name] = r
             if "poly_ntt" in row and "mul_ntt" in row:
                 # Poly = 4 products but 10 (not 12) transforms per prime (squarings)
@@ -584,10 +588,11 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_source"] = peaks["source"] if roof["bound"] == "hbm" else \
         "derived: measured int-pipe rates (profiles/r01_int_peak.jsonl) x sm_max_mhz"
-    nc = load_ncu(roof["kernel"], bits)
+    nc = load_ncu(dom, bits)
     roof["traffic"] = nc.get("dram_bytes") if nc else None
     if nc:
-        roof["ncu"] = {k: nc[k] for k in ("fmaheavy_pct", "alu_pct", "issue_pct", "source") if k in nc}
+        roof["ncu"] = {k: nc[k] for k in ("kernel", "fmaheavy_pct", "alu_pct", "issue_pct", "duration_us", "source")
+                       if k in nc}
     roof["share_of_step"] = op_ms[dom] / ms
 
     line = {
