@@ -425,6 +425,39 @@ def per_size(args, bn, inputs, torch, dev, stream, rk, peaks, shard):
         out["262144_ONES"] = row
         del a1, o
         torch.cuda.empty_cache()
+    # beyond one CTA: thread-block clusters (512K, 1M) and the
+    # decoupled look-back add (4M, 64M bits; 64M also on the all-carry RIPPLE class)
+    beyond = {}
+    for bits, ops_b, cls in ((1 << 19, ("add", "mul_ntt", "add_big"), args.cls),
+                             (1 << 20, ("add", "mul_ntt", "add_big"), args.cls),
+                             (1 << 22, ("add_big",), args.cls), (1 << 26, ("add_big",), args.cls),
+                             (1 << 26, ("add_big",), "RIPPLE")):
+        m = bits // 32
+        n_job = (1 << 32) // bits
+        lo, hi, total = shard.plan(rk.rank, rk.world, n_job if args.scaling == "weak" else n_job * rk.world,
+                                   args.scaling)
+        x, y = inputs.make_operands(hi - lo, m, seed=1, cls=cls, inst0=lo, device=dev)
+        o = torch.empty_like(x)
+        wsb = bn.add_big_workspace(x)
+        key = str(bits) + ("" if cls == args.cls else "_" + cls)
+        row = {"instances": total, "input_class": cls}
+        for name in ops_b:
+            f = (lambda: bn.add_big(x, y, out=o, workspace=wsb)) if name == "add_big" else \
+                (lambda name=name: getattr(bn, name)(x, y, out=o))
+            rk.barrier()
+            st = stats(time_op(torch, f, stream))
+            ms = rk.max(st["ms"])
+            r = {"ms": ms, "ms_median": rk.max(st["ms_median"]), "reps": st["reps"]}
+            if name in ("add", "add_big"):
+                r["GB/s"] = total * work(bits)["add_bytes"] / (ms * 1e-3) / 1e9
+                r["frac_hbm"] = r["GB/s"] / rk.world / peaks["hbm_gbs"]
+            else:
+                r["mults/s"] = total / (ms * 1e-3)
+            row[name] = r
+        beyond[key] = row
+        del x, y, o, wsb
+        torch.cuda.empty_cache()
+    out["beyond_one_cta"] = beyond
     # C3: classical vs NTT crossover (first size where the NTT product is faster)
     cross = next((b for b in SIZES if out[str(b)]["mul_ntt"]["ms"] < out[str(b)]["mul_classical"]["ms"]), None)
     meta = {"timing": "per (op, size): 3 warm-ups (1 for classical-type ops >= 64K), then back-to-back "

@@ -139,6 +139,26 @@ bn_status bn_poly_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
                       uint32_t n_limbs, uint32_t limb_bits, void *workspace,
                       uint64_t workspace_bytes, bn_stream_t stream);
 
+/* ---- addition beyond one cluster ------------------------
+ * bn_add_big — out[k] = (a[k] + b[k]) mod 2^bits, like bn_add, for any
+ * power-of-two size from 2^18 to 2^30 bits, with the single-pass
+ * decoupled look-back carry scan the paper's scan citation refers to
+ * (PAPER.md:66, 289-292): every instance is cut into tiles of 2^18 bits, one
+ * CTA per tile, tiles taken in order from an atomic counter; each tile
+ * publishes its carry aggregate, looks back over its predecessors' flags for
+ * its carry-in, and publishes its carry-out.  Same layout,
+ * alignment, aliasing and stream rules as bn_add; n_inst * bits / 2^18 must
+ * be < 2^31 (else BN_ESIZE).
+ * workspace: DEVICE buffer of at least bn_add_big_workspace_bytes(...) bytes
+ * (one 32-bit flag per tile + a counter), 16-byte aligned, owned by the
+ * caller, not overlapping a, b or out, not shared with a concurrent call;
+ * the call zeroes it on `stream` (cudaMemsetAsync) before the kernel.
+ * Too small -> BN_EINVAL. */
+bn_status bn_add_big(void *out, const void *a, const void *b, uint64_t n_inst, uint32_t n_limbs,
+                     uint32_t limb_bits, void *workspace, uint64_t workspace_bytes, bn_stream_t stream);
+/* Workspace bytes bn_add_big needs; 0 for n_inst == 0 or an invalid size. */
+uint64_t bn_add_big_workspace_bytes(uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits);
+
 /* Workspace bytes a bn_poly_* call needs on the CURRENT device for this
  * batch (one slice of 3 intermediates per resident CTA; <= 3 * n_inst *
  * bits / 8).  op = BN_OP_POLY_CLASSICAL or BN_OP_POLY_NTT.  Returns 0 for

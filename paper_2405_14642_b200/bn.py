@@ -67,6 +67,8 @@ def load():
                 "bn_poly_classical": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
                 "bn_poly_ntt": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
                 "bn_poly_workspace_bytes": ([i32, u64, u32, u32], u64),
+                "bn_add_big": ([vp, vp, vp, u64, u32, u32, vp, u64, vp], i32),
+                "bn_add_big_workspace_bytes": ([u64, u32, u32], u64),
                 "bn_prepare": ([i32], i32),
                 "bn_run_host": ([ctypes.POINTER(i32), ctypes.POINTER(vp), i32, vp, vp, u64, u32, u32], i32),
                 "bn_max_bits": ([], u32),
@@ -194,8 +196,35 @@ def mul_wide_classical(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tens
 
 
 def mul_wide_ntt(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
-    """Full product a * b (2 n_limbs limbs per instance), exact NTT; bits <= 131072."""
+    """Full product a * b (2 n_limbs limbs per instance), exact NTT; bits <= 262144."""
     return _wide("bn_mul_wide_ntt", a, b, out)
+
+
+ADD_BIG_MIN_BITS, ADD_BIG_MAX_BITS = 1 << 18, 1 << 30
+
+
+def add_big_workspace(a: torch.Tensor) -> torch.Tensor:
+    """A workspace tensor for add_big on a's device (tile flags + counter)."""
+    nb = int(load().bn_add_big_workspace_bytes(a.shape[0], a.shape[1], _limb_bits(a)))
+    return torch.empty(max(16, nb), dtype=torch.uint8, device=a.device)
+
+
+def add_big(a: torch.Tensor, b: torch.Tensor, out=None, workspace=None) -> torch.Tensor:
+    """(a + b) mod 2^bits for 2^18 .. 2^30-bit instances, decoupled look-back
+    carry scan over 2^18-bit tiles (bn_add_big)."""
+    out = _check(a, b, out)
+    if workspace is None:
+        workspace = add_big_workspace(a)
+    if not workspace.is_cuda or workspace.device != a.device or not workspace.is_contiguous():
+        raise ValueError("workspace must be a contiguous CUDA tensor on the operands' device")
+    lib = load()
+    n_inst, n_limbs = a.shape
+    with _on_device(a.device) as stream:
+        st = lib.bn_add_big(out.data_ptr(), a.data_ptr(), b.data_ptr(), n_inst, n_limbs, _limb_bits(a),
+                            workspace.data_ptr(), workspace.numel() * workspace.element_size(), stream)
+    if st != 0:
+        raise BnError(st, "bn_add_big")
+    return out
 
 
 def add6(a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:

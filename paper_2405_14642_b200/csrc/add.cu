@@ -174,6 +174,120 @@ __global__ void __launch_bounds__(1024, MB)
   if constexpr (NS > 0) cp_async_wait<0>();
 }
 
+// ------------------------------------------------------------ beyond clusters
+// bn_add_big: any power-of-two size from 2^18 to 2^30 bits with the
+// single-pass decoupled look-back scan the paper's carry-scan citation refers
+// to — the way past what one CTA (2^18) or one
+// thread-block cluster (2^20) can hold.  Every instance is cut into tiles of
+// 8192 limbs (2^18 bits; 1024 threads x 8 limbs, loaded straight into
+// registers); CTAs take tiles in order from an atomic counter, so every
+// tile's predecessors have started (no deadlock whatever the scheduling).
+// A tile publishes its aggregate (g = carry-out with carry-in 0, p = every
+// limb sum all ones) as soon as its CTA scan is done, looks back for its
+// carry-in, then publishes its inclusive carry-out.  For the carry operator
+// the look-back is short: a predecessor with p = 0 is already decisive
+// (carry = g, whatever came into it), only all-ones tiles pass the carry on.
+// One warp reads 32 predecessors' flags at once and takes the nearest
+// decisive one (an instance's first tile has carry-in 0).  Flag word:
+// bits 0-1 status (0 none, 1 aggregate, 2 inclusive), bit 2 g, bit 3 p,
+// bit 4 inclusive carry-out; payload and status in one 32-bit store, so no
+// fence is needed between them.  Flags and the counter live in a caller
+// workspace zeroed (cudaMemsetAsync) before the launch.
+constexpr int kLbThreads = 1024, kLbL = 8, kLbTile = kLbThreads * kLbL;  // 8192 limbs per tile
+
+BN_DEV uint32_t ld_flag(const uint32_t* f) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+BN_DEV void st_flag(uint32_t* f, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kLbThreads, 2)
+    add_lookback_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t total_tiles,
+                        uint32_t tiles_per_inst, uint32_t* flags, uint32_t* counter) {
+  __shared__ uint32_t tile_s, cin_s;
+  __shared__ uint32_t agg[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) tile_s = atomicAdd(counter, 1u);
+  __syncthreads();
+  const uint64_t tile = tile_s;
+  if (tile >= total_tiles) return;
+  const uint32_t lt = (uint32_t)(tile % tiles_per_inst);  // tile index within its instance
+  const uint64_t off = tile * (uint64_t)kLbTile + tid * kLbL;  // instances are contiguous
+  uint32_t x[kLbL], y[kLbL], r[kLbL], g, p;
+  load_limbs<kLbL>(x, a + off);
+  load_limbs<kLbL>(y, b + off);
+  chunk_sum<kLbL>(x, y, r, g, p);
+  // lane and warp levels (ballot-add), as in carry_scan / cluster_carry_scan
+  const uint32_t G = __ballot_sync(0xFFFFFFFFu, g), P = __ballot_sync(0xFFFFFFFFu, p), X = G | P;
+  if (lane == 0) agg[warp] = (uint32_t)(((uint64_t)X + G) >> 32) | ((P == 0xFFFFFFFFu) << 1);
+  __syncthreads();
+  const uint32_t av = agg[lane];
+  const uint32_t G2 = __ballot_sync(0xFFFFFFFFu, av & 1u), P2 = __ballot_sync(0xFFFFFFFFu, (av >> 1) & 1u);
+  const uint32_t X2 = G2 | P2;
+  if (warp == 0) {
+    const uint32_t gT = (uint32_t)(((uint64_t)X2 + G2) >> 32), pT = P2 == 0xFFFFFFFFu;
+    uint32_t C = 0;
+    if (lt == 0) {
+      if (lane == 0) st_flag(flags + tile, 2u | (gT << 2) | (pT << 3) | (gT << 4));
+    } else {
+      if (lane == 0) st_flag(flags + tile, 1u | (gT << 2) | (pT << 3));
+      // look back over the instance's earlier tiles, 32 at a time
+      uint64_t base = tile;  // window: base-1-lane
+      uint32_t remaining = lt;  // earlier tiles of this instance
+      for (;;) {
+        const bool in = lane < remaining;
+        uint32_t f = 0;
+        if (in) {
+          do {
+            f = ld_flag(flags + base - 1 - lane);
+          } while ((f & 3u) == 0);
+        }
+        // decisive: inclusive published, or an aggregate that kills / generates (p = 0);
+        // lanes past the instance's first tile count as decisive with carry 0
+        const bool dec = !in || (f & 3u) == 2u || !((f >> 3) & 1u);
+        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dec);
+        if (dm) {
+          const int d = __ffs(dm) - 1;
+          const uint32_t fd = __shfl_sync(0xFFFFFFFFu, f, d);
+          const bool ind = d < (int)remaining;
+          C = !ind ? 0u : ((fd & 3u) == 2u ? (fd >> 4) & 1u : (fd >> 2) & 1u);
+          break;
+        }
+        base -= 32;
+        remaining -= 32;
+      }
+      if (lane == 0) st_flag(flags + tile, 2u | (gT << 2) | (pT << 3) | ((gT | (pT & C)) << 4));
+    }
+    if (lane == 0) cin_s = C;
+  }
+  __syncthreads();
+  const uint32_t C = cin_s;
+  const uint32_t c0 = (((X2 + G2 + C) ^ X2 ^ G2) >> warp) & 1u;
+  const uint32_t cin = (((X + G + c0) ^ X ^ G) >> lane) & 1u;
+  chunk_apply<kLbL>(x, r, cin);
+  store_limbs<kLbL>(out + off, r);
+}
+
+uint64_t add_big_workspace_words(int logm, uint64_t n_inst) {
+  const uint64_t tiles = n_inst * ((1ull << logm) / kLbTile);
+  return (tiles + 1 + 3) & ~3ull;  // flags + counter, 16-byte multiple
+}
+
+cudaError_t launch_add_big(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                           uint32_t* ws, uint64_t ws_words, cudaStream_t st) {
+  const uint32_t tpi = (uint32_t)((1ull << logm) / kLbTile);
+  const uint64_t total = n_inst * tpi;
+  if (tpi < 1 || total >= (1ull << 31) || ws_words < add_big_workspace_words(logm, n_inst))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(ws, 0, (total + 1) * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  add_lookback_kernel<<<(unsigned)total, kLbThreads, 0, st>>>(out, a, b, total, tpi, ws + 1, ws);
+  return cudaGetLastError();
+}
+
 template <int LOGM, int L = 8, int NS = BN_ADD_CL_STAGES, int MB = 1>
 static cudaError_t launch_add_cluster_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                         cudaStream_t st, int n_sm) {

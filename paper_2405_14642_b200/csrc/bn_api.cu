@@ -23,6 +23,8 @@ thread_local int tls_cuda_err = 0;
 
 constexpr int kMaxDev = 64;
 constexpr uint32_t kMinBits = 1024, kMaxBits = 1048576;
+// bn_add_big: 2^18 .. 2^30 bits (tiles of 2^18 bits, decoupled look-back)
+constexpr int kBigMinLb = 18, kBigMaxLb = 30;
 
 // Largest log2(bits) per operation: 2^18 fits one CTA (the paper's range);
 // add and the NTT product go to 2^20, the classical product to 2^19, on
@@ -415,6 +417,43 @@ bn_status bn_poly_ntt(void* out, const void* a, const void* b, uint64_t n_inst, 
                       uint32_t limb_bits, void* workspace, uint64_t workspace_bytes, bn_stream_t stream) {
   return run_poly(BN_OP_POLY_NTT, out, a, b, n_inst, n_limbs, limb_bits, workspace, workspace_bytes,
                   (cudaStream_t)stream);
+}
+
+uint64_t bn_add_big_workspace_bytes(uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits) {
+  if (limb_bits != 32 && limb_bits != 64) return 0;
+  const int lb = ilog2_exact((uint64_t)n_limbs * limb_bits);
+  if (lb < kBigMinLb || lb > kBigMaxLb || n_inst == 0) return 0;
+  return bn::add_big_workspace_words(lb - 5, n_inst) * 4;
+}
+
+bn_status bn_add_big(void* out, const void* a, const void* b, uint64_t n_inst, uint32_t n_limbs, uint32_t limb_bits,
+                     void* workspace, uint64_t workspace_bytes, bn_stream_t stream) {
+  if (limb_bits != 32 && limb_bits != 64) return BN_EINVAL;
+  if (n_limbs == 0) return BN_EINVAL;
+  const uint64_t bits = (uint64_t)n_limbs * limb_bits;
+  const int lb = ilog2_exact(bits);
+  if (lb < kBigMinLb || lb > kBigMaxLb) return BN_ESIZE;
+  if (n_inst == 0) return BN_OK;
+  if (!out || !a || !b || !workspace) return BN_EINVAL;
+  if (((uintptr_t)out | (uintptr_t)a | (uintptr_t)b | (uintptr_t)workspace) & 15) return BN_EALIGN;
+  const uint64_t bytes = n_inst * (bits / 8);
+  if (n_inst * (bits >> 18) >= (1ull << 31)) return BN_ESIZE;  // tiles of 2^18 bits, int32 grid
+  const uint64_t need = bn::add_big_workspace_words(lb - 5, n_inst) * 4;
+  if (workspace_bytes < need) return BN_EINVAL;
+  auto overl = [](const void* x, uint64_t xn, const void* y, uint64_t yn) {
+    const uintptr_t x0 = (uintptr_t)x, y0 = (uintptr_t)y;
+    return x0 < y0 + yn && y0 < x0 + xn;
+  };
+  auto partial = [&](const void* x, const void* y) { return x != y && overl(x, bytes, y, bytes); };
+  if (partial(out, a) || partial(out, b)) return BN_EALIAS;
+  if (overl(workspace, need, out, bytes) || overl(workspace, need, a, bytes) || overl(workspace, need, b, bytes))
+    return BN_EALIAS;
+  DevState* d = nullptr;
+  bn_status s = current_device(&d);
+  if (s != BN_OK) return s;
+  cudaError_t e = bn::launch_add_big(lb - 5, (uint32_t*)out, (const uint32_t*)a, (const uint32_t*)b, n_inst,
+                                     (uint32_t*)workspace, need / 4, (cudaStream_t)stream);
+  return e == cudaSuccess ? BN_OK : cuda_fail(e);
 }
 
 bn_status bn_prepare(int device) {

@@ -92,6 +92,11 @@ cudaError_t launch_mul_classical(int logm, uint32_t* out, const uint32_t* a, con
                                  uint64_t n_inst, cudaStream_t st, int n_sm);
 cudaError_t launch_mul_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                            uint64_t n_inst, const NttTables& tb, cudaStream_t st, int n_sm);
+// add beyond the cluster sizes (decoupled look-back over 8192-limb tiles),
+// logm 13 .. 25; the workspace (flags + tile counter) is zeroed per launch
+uint64_t add_big_workspace_words(int logm, uint64_t n_inst);
+cudaError_t launch_add_big(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                           uint32_t* ws, uint64_t ws_words, cudaStream_t st);
 // Fused workloads: 6-Add and Poly.  The Poly kernels use
 // a caller-provided workspace of ws_words u32 words, sized by *_geometry for
 // the same (logm, n_inst, n_sm) — one slice per resident CTA.
@@ -105,7 +110,7 @@ cudaError_t poly_ntt_geometry(int logm, uint64_t n_inst, int n_sm, uint64_t* ws_
 cudaError_t launch_poly_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                             const NttTables& tb, uint32_t* ws, uint64_t ws_words, cudaStream_t st, int n_sm);
 // Full (untruncated) products: out has 2^(logm+1) u32 limbs per instance.
-// The NTT version supports logm <= 12 (inputs up to 128K bits).
+// Both support logm <= 13 (inputs up to 256K bits).
 cudaError_t launch_mul_wide_classical(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,
                                       uint64_t n_inst, cudaStream_t st, int n_sm);
 cudaError_t launch_mul_wide_ntt(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b,

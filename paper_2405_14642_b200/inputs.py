@@ -67,8 +67,10 @@ def _hash_grid(seed: int, operand: int, inst0: int, n_inst: int, m: int, device)
     limb = torch.arange(m, dtype=torch.int64, device=device).view(1, -1)
     if m <= 8192:
         ctr = (inst << 14) | limb  # m <= 8192 < 2^14
-    else:  # cluster sizes: m <= 32768 < 2^16, separate counter domain (bit 62)
+    elif m <= 32768:  # cluster sizes: m < 2^16, separate counter domain (bit 62)
         ctr = (inst << 16) | limb | (1 << 62)
+    else:  # bn_add_big sizes: m <= 2^25 < 2^26, another domain (bit 61)
+        ctr = (inst << 26) | limb | (1 << 61)
     return _lsr(splitmix64(ctr ^ _key(seed, operand)), 32)
 
 
@@ -115,8 +117,8 @@ def make_operands(n_inst: int, m: int, seed: int = 1, cls: str = "U", inst0: int
     sharding of the instance range."""
     if cls not in CLASSES:
         raise ValueError("unknown input class %r (one of %s)" % (cls, CLASSES))
-    if m < 1 or m > 32768:
-        raise ValueError("m must be in [1, 32768]")
+    if m < 1 or m > (1 << 25):
+        raise ValueError("m must be in [1, 2^25]")
     if n_inst == 0:
         z = torch.zeros((0, m), dtype=torch.int32, device=device)
         return z, z.clone()

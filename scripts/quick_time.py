@@ -25,7 +25,8 @@ for bits in [int(x) for x in args.bits.split(",")]:
     o1 = torch.empty_like(a)
     o2 = torch.empty((n, 2 * m), dtype=a.dtype, device=dev)
     for op in args.ops.split(","):
-        if bits > bn.max_bits(op):
+        top = bn.ADD_BIG_MAX_BITS if op == "add_big" else bn.max_bits(op)
+        if bits > top:
             continue
         f = getattr(bn, op)
         o = o2 if "wide" in op else o1

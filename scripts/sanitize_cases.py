@@ -17,7 +17,7 @@ bn.prepare(0)
 bad = 0
 cases = [(1024, 37), (2048, 41), (4096, 19), (65536, 3), (131072, 2), (262144, 1)]
 if "--big" in sys.argv:
-    cases += [(1 << 19, 2), (1 << 20, 1)]
+    cases += [(1 << 19, 2), (1 << 20, 1), (1 << 22, 2)]
 for cap in (0, 2):
     bn.debug_set_grid_cap(cap)
     for bits, n in cases:
@@ -25,8 +25,13 @@ for cap in (0, 2):
         a, b = inputs.make_operands(n, m, seed=bits + cap, cls="MIX")
         an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
         da, db = a.to(dev), b.to(dev)
-        want = {"add": O.add(an, bnp), "mul": O.mul(an, bnp, nthreads=8)}
-        ops = [("add", bn.add), ("mul", bn.mul_ntt)]
+        want = {"add": O.add(an, bnp)}
+        ops = []
+        if bits <= bn.max_bits("add"):
+            ops += [("add", bn.add)]
+        if bits <= bn.max_bits("mul_ntt"):
+            want["mul"] = O.mul(an, bnp, nthreads=8)
+            ops += [("mul", bn.mul_ntt)]
         if bits <= bn.max_bits("mul_classical"):
             ops += [("mul", bn.mul_classical)]
         if bits <= 262144:
@@ -35,6 +40,8 @@ for cap in (0, 2):
             want["wide"] = O.mul_full_rows(an, bnp)
             ops += [("add6", bn.add6), ("poly", bn.poly_classical), ("poly", bn.poly_ntt),
                     ("wide", bn.mul_wide_classical), ("wide", bn.mul_wide_ntt)]
+        if bits >= (1 << 18):
+            ops += [("add", bn.add_big)]
         for key, f in ops:
             got = inputs.to_numpy_u32(f(da, db))
             torch.cuda.synchronize()

@@ -168,3 +168,24 @@ def test_build_stamp_tracks_flags():
     _build.build()
     assert _build.up_to_date()
     assert not _build.up_to_date(_build.LIB, extra=("-DBN_SOME_VARIANT=1",))
+
+
+def test_add_big_validation_before_launch(lib):
+    """bn_add_big argument checks return before any launch (no GPU needed)."""
+    f = lib.bn_add_big
+    A, B, O, W = 0x10000, 0x20000000, 0x40000000, 0x60000000
+    m = 1 << 16  # 2^21 bits
+    ws = lib.bn_add_big_workspace_bytes(3, m, 32)
+    assert ws == 4 * ((3 * 8 + 1 + 3) // 4 * 4)  # one flag per 2^18-bit tile + counter, 16-byte multiple
+    assert lib.bn_add_big_workspace_bytes(0, m, 32) == 0
+    assert lib.bn_add_big_workspace_bytes(3, 1 << 12, 32) == 0      # 2^17 bits: below the range
+    assert lib.bn_add_big_workspace_bytes(3, 1 << 26, 32) == 0      # 2^31 bits: above
+    assert f(O, A, B, 3, 1 << 12, 32, W, ws, None) == 2             # BN_ESIZE
+    assert f(O, A, B, 3, 3 << 14, 32, W, ws, None) == 2             # not a power of two
+    assert f(O, A, B, 3, m, 16, W, ws, None) == 1                   # limb_bits
+    assert f(O, A, B, 0, m, 32, W, ws, None) == 0                   # n_inst == 0: nothing to do
+    assert f(O, A, B, 3, m, 32, 0, ws, None) == 1                   # no workspace
+    assert f(O, A, B, 3, m, 32, W, ws - 16, None) == 1              # workspace too small
+    assert f(O + 4, A, B, 3, m, 32, W, ws, None) == 3               # alignment
+    assert f(A + 16, A, B, 3, m, 32, W, ws, None) == 4              # partial overlap
+    assert f(O, A, B, 3, m, 32, O + 64, ws, None) == 4              # workspace overlaps out

@@ -576,3 +576,56 @@ def test_wide_ntt_256k_grid_cap(cap):
     exp[m] = -2
     exp[m + 1:] = -1
     assert torch.equal(w, exp.expand(3, 2 * m))
+
+
+# ------------------------- beyond clusters: decoupled look-back (§8(f) #4)
+
+@pytest.mark.parametrize("cls", ["U", "ONES", "RIPPLE", "RUNS", "MIX"])
+@pytest.mark.parametrize("bits", [1 << 18, 1 << 20, 1 << 21, 1 << 23])
+def test_parity_add_big(bits, cls):
+    """bn_add_big (tiles of 2^18 bits, decoupled look-back carry scan) vs the
+    oracle, bit-exact: RIPPLE carries through every tile of an instance, ONES
+    makes every tile all-propagate (the look-back walks back to a decisive
+    tile); at 2^18 .. 2^20 also equal to bn_add (one CTA / cluster)."""
+    m = bits // 32
+    n = 5 if bits <= (1 << 21) else 2
+    a, b = inputs.make_operands(n, m, seed=bits % 977 + len(cls), cls=cls)
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    da, db = a.to(DEV), b.to(DEV)
+    got = bn.add_big(da, db)
+    bad = _first_bad(inputs.to_numpy_u32(got), O.add(an, bnp))
+    assert bad is None, "add_big %d %s: %s" % (bits, cls, bad)
+    if bits <= bn.max_bits("add"):
+        assert torch.equal(got, bn.add(da, db))
+
+
+def test_add_big_worst_case_chain_and_in_place():
+    """2^26-bit instances (256 tiles each), a = 2^B - 1, b = 1: one carry
+    through every limb of every tile; in place (out == a) too; and a batch
+    whose instance boundaries cut the look-back (instance k's first tile must
+    not take instance k-1's carry, reading R1)."""
+    bits = 1 << 26
+    m = bits // 32
+    ones, _ = inputs.make_operands(3, m, seed=1, cls="ONES", device=DEV)
+    one = torch.zeros((3, m), dtype=torch.int32, device=DEV)
+    one[:, 0] = 1
+    assert not bn.add_big(ones, one).any()               # (2^B - 1) + 1 = 0 mod 2^B, every instance
+    s = bn.add_big(ones, ones, out=ones)                  # in place: 2^(B+1) - 2 mod 2^B
+    want = torch.full((m,), -1, dtype=torch.int32, device=DEV)
+    want[0] = -2
+    assert torch.equal(s, want.expand(3, m))
+
+
+@pytest.mark.parametrize("bits", [1 << 22])
+def test_add_big_u64_and_paper_batch(bits):
+    """u64 limbs are the same bytes; the paper batch (2^32 bits per operand)
+    sampled against the oracle."""
+    m = bits // 32
+    n = (1 << 32) // bits
+    a, b = inputs.make_operands(n, m, seed=9, cls="MIX", device=DEV)
+    r32 = bn.add_big(a, b)
+    r64 = bn.add_big(a.view(torch.int64), b.view(torch.int64)).view(torch.int32)
+    assert torch.equal(r32, r64)
+    idx = torch.tensor([0, n // 2, n - 1], device=DEV)
+    want = O.add(inputs.to_numpy_u32(a[idx]), inputs.to_numpy_u32(b[idx]))
+    assert np.array_equal(inputs.to_numpy_u32(r32[idx]), want)
