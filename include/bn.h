@@ -143,11 +143,12 @@ bn_status bn_poly_ntt(void *out, const void *a, const void *b, uint64_t n_inst,
  * bn_add_big — out[k] = (a[k] + b[k]) mod 2^bits, like bn_add, for any
  * power-of-two size from 2^18 to 2^30 bits, with the single-pass
  * decoupled look-back carry scan the paper's scan citation refers to
- * (PAPER.md:66, 289-292): every instance is cut into tiles of 2^18 bits, one
- * CTA per tile, tiles taken in order from an atomic counter; each tile
+ * (PAPER.md:66, 289-292): every instance is cut into fixed-size tiles (at
+ * most 2^18 bits; bn_config.h), one CTA per tile, tiles taken in order from
+ * an atomic counter; each tile
  * publishes its carry aggregate, looks back over its predecessors' flags for
  * its carry-in, and publishes its carry-out.  Same layout,
- * alignment, aliasing and stream rules as bn_add; n_inst * bits / 2^18 must
+ * alignment, aliasing and stream rules as bn_add; the number of tiles must
  * be < 2^31 (else BN_ESIZE).
  * workspace: DEVICE buffer of at least bn_add_big_workspace_bytes(...) bytes
  * (one 32-bit flag per tile + a counter), 16-byte aligned, owned by the

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(1024, MB)
 // bit 4 inclusive carry-out; payload and status in one 32-bit store, so no
 // fence is needed between them.  Flags and the counter live in a caller
 // workspace zeroed (cudaMemsetAsync) before the launch.
-constexpr int kLbThreads = 1024, kLbL = 8, kLbTile = kLbThreads * kLbL;  // 8192 limbs per tile
+constexpr int kLbThreads = BN_ADD_BIG_THREADS, kLbL = 8, kLbTile = kLbThreads * kLbL;  // limbs per tile
 
 BN_DEV uint32_t ld_flag(const uint32_t* f) {
   uint32_t v;
@@ -204,12 +204,13 @@ BN_DEV void st_flag(uint32_t* f, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kLbThreads, 2)
+__global__ void __launch_bounds__(kLbThreads, 2048 / kLbThreads)
     add_lookback_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t total_tiles,
                         uint32_t tiles_per_inst, uint32_t* flags, uint32_t* counter) {
   __shared__ uint32_t tile_s, cin_s;
   __shared__ uint32_t agg[32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 32) agg[tid] = 2u;  // warps past the CTA's count: the operator's identity (g 0, p 1)
   if (tid == 0) tile_s = atomicAdd(counter, 1u);
   __syncthreads();
   const uint64_t tile = tile_s;

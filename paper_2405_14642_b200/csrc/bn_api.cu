@@ -437,8 +437,8 @@ bn_status bn_add_big(void* out, const void* a, const void* b, uint64_t n_inst, u
   if (!out || !a || !b || !workspace) return BN_EINVAL;
   if (((uintptr_t)out | (uintptr_t)a | (uintptr_t)b | (uintptr_t)workspace) & 15) return BN_EALIGN;
   const uint64_t bytes = n_inst * (bits / 8);
-  if (n_inst * (bits >> 18) >= (1ull << 31)) return BN_ESIZE;  // tiles of 2^18 bits, int32 grid
   const uint64_t need = bn::add_big_workspace_words(lb - 5, n_inst) * 4;
+  if (need / 4 >= (1ull << 31)) return BN_ESIZE;  // one CTA per tile: the grid is an int32
   if (workspace_bytes < need) return BN_EINVAL;
   auto overl = [](const void* x, uint64_t xn, const void* y, uint64_t yn) {
     const uintptr_t x0 = (uintptr_t)x, y0 = (uintptr_t)y;
