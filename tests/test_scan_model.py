@@ -253,3 +253,60 @@ def test_six_add_carry_save_model(L, n_chunks):
         for k in range(1, 6):
             want = (want + (a if k % 2 else b)) % mod
         assert _six_add_carry_save(a, b, n_chunks, L) == want, (hex(a), hex(b))
+
+
+def _lookback_carry(tile, lt, flags):
+    """Model of add_lookback_kernel's warp-wide look-back (add.cu): window of
+    32 predecessors, lane k reads tile - 1 - k (lanes at or past the
+    instance's first tile are decisive with carry 0); a predecessor is
+    decisive if its inclusive carry is published (status 2) or its aggregate
+    does not propagate (p = 0, carry = g); the nearest decisive one wins."""
+    base, remaining = tile, lt
+    while True:
+        lanes = []
+        for k in range(32):
+            if k < remaining:
+                st, g, p, inc = flags[base - 1 - k]
+                assert st != 0, "the kernel spins until a flag is published"
+                dec = st == 2 or p == 0
+                lanes.append((dec, (inc if st == 2 else g)))
+            else:
+                lanes.append((True, 0))
+        ds = [k for k, (d, _) in enumerate(lanes) if d]
+        if ds:
+            return lanes[ds[0]][1] if ds[0] < remaining else 0
+        base -= 32
+        remaining -= 32
+
+
+@pytest.mark.parametrize("tiles_per_inst", [1, 5, 33, 70])
+def test_decoupled_lookback_model(tiles_per_inst):
+    """The look-back decision equals the sequential carry into every tile
+    (carry_op of PAPER.md:177-215 folded from the instance's first tile), for
+    tiles that are all-propagate for long stretches (> 32, so the window
+    slides) and any mix of published aggregate / inclusive flags; carries
+    never cross an instance boundary (reading R1)."""
+    import random
+    rng = random.Random(tiles_per_inst)
+    n_inst = 3
+    for trial in range(200):
+        aggs = []
+        for i in range(n_inst * tiles_per_inst):
+            r = rng.random()
+            if trial % 3 == 0:
+                g, p = (0, 1) if rng.random() < 0.95 else (rng.randrange(2), 0)  # long propagate runs
+            else:
+                g, p = (1, 0) if r < 0.3 else (0, 0) if r < 0.6 else (0, 1)
+            aggs.append((g, p))
+        # true carries: fold within each instance
+        true_cin, incl = [], []
+        for i, (g, p) in enumerate(aggs):
+            c = 0 if i % tiles_per_inst == 0 else incl[-1]
+            true_cin.append(c)
+            incl.append(g | (p & c))
+        # every tile's aggregate is published; a random subset also has its inclusive flag
+        flags = [(2 if rng.random() < 0.5 else 1, g, p, incl[i]) for i, (g, p) in enumerate(aggs)]
+        for t in range(len(aggs)):
+            lt = t % tiles_per_inst
+            got = 0 if lt == 0 else _lookback_carry(t, lt, flags)
+            assert got == true_cin[t], (trial, t)
