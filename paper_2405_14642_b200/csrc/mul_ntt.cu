@@ -947,69 +947,66 @@ __global__ void __launch_bounds__(NttR32Cfg<LOGN>::T, NttR32Cfg<LOGN>::MINB)
   constexpr int N = C::N, M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* X = sm;              // plane 0 | plane 1 (N words each)
-  uint32_t* Res = sm + 2 * N;    // 3 M residues (last product), cswz<16>
-  uint32_t* agg = Res + 3 * M;   // T / 32
+  uint32_t* Park = sm + 2 * N;   // A-hat parked here (the 1-Mul kernel's residue area)
+  uint32_t* agg = Park + 3 * M;  // T / 32
   const int t = threadIdx.x;
   uint32_t* G9 = ws + (uint64_t)blockIdx.x * PolyR32Cfg<LOGN>::WS_WORDS;  // [3 P + j][M]
   uint32_t* t1 = G9 + 9 * M;
   uint32_t* t2 = t1 + M;
   uint32_t* t3 = t2 + M;
   for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x) {
-    const uint32_t* ai = a + inst * M;
-    const uint32_t* bi = b + inst * M;
-    // first level: A-hat, B-hat once per prime, three inverse transforms
+    // Two phases through ONE copy of the transform code (phase 0: the three
+    // first-level products of a, b; phase 1: t1 * t2), so ptxas allocates
+    // registers for a single transform body (two inlined bodies spilled
+    // 430-560 bytes per thread).  Every product's residues go to the
+    // workspace (G9), every epilogue reads them from there.
 #pragma unroll 1
-    for (int j = 0; j < kNumPrimes; j++) {
-      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
-      const uint2* twf = tw + (2 * j + 0) * (N - 1);
-      const uint2* twi = tw + (2 * j + 1) * (N - 1);
-      uint32_t xab[2][32];
-      r32_load<LOGN, false>(xab, ai, bi, t, p2);
-      r32_fwd<LOGN>(xab, X, t, twf, p, p2);
-      // park A-hat in the (idle) residue area and B-hat in plane 1, which the
-      // one-vector inverse exchanges never touch; thread-private slots
-      // [e T + t], read back only by their owner
-      __syncthreads();  // every read of plane 1 by the last forward exchange is done
+    for (int phase = 0; phase < 2; phase++) {
+      const uint32_t* xi = phase ? t1 : a + inst * M;
+      const uint32_t* yi = phase ? t2 : b + inst * M;
+      const int P0 = phase ? 2 : 0;  // phase 1: the single product t1 * t2, into G9 slot 2
+#pragma unroll 1
+      for (int j = 0; j < kNumPrimes; j++) {
+        const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
+        const uint2* twf = tw + (2 * j + 0) * (N - 1);
+        const uint2* twi = tw + (2 * j + 1) * (N - 1);
+        {
+          uint32_t xab[2][32];
+          r32_load<LOGN, true>(xab, xi, yi, t, p2);
+          r32_fwd<LOGN>(xab, X, t, twf, p, p2);
+          // park A-hat in the residue area and B-hat in plane 1, which the
+          // one-vector inverse exchanges never touch; thread-private slots
+          // [e T + t], read back only by their owner
+          __syncthreads();  // every read of plane 1 by the last forward exchange is done
 #pragma unroll
-      for (int e = 0; e < 32; e++) {
-        Res[e * C::T + t] = xab[0][e];
-        X[N + e * C::T + t] = xab[1][e];
+          for (int e = 0; e < 32; e++) {
+            Park[e * C::T + t] = xab[0][e];
+            X[N + e * C::T + t] = xab[1][e];
+          }
+        }
+#pragma unroll 1
+        for (int P = P0; P < 3; P++) {
+          // P = 0: A-hat^2, 1: B-hat^2, 2: A-hat B-hat
+          const uint32_t* U = (P == 1 ? X + N : Park) + t;
+          const uint32_t* V = (P == 0 ? Park : X + N) + t;
+          uint32_t x[1][32];
+#pragma unroll
+          for (int e = 0; e < 32; e++) x[0][e] = mont(U[e * C::T], V[e * C::T], p, pinv);
+          r32_inv<LOGN>(x, X, t, twi, p, p2);
+          uint32_t* g = G9 + (3 * P + j) * M;
+#pragma unroll
+          for (int e = 0; e < 16; e++) g[t + e * (N / 32)] = x[0][e];
+        }
       }
-#pragma unroll 1
-      for (int P = 0; P < 3; P++) {
-        // P = 0: A-hat^2, 1: B-hat^2, 2: A-hat B-hat
-        const uint32_t* U = (P == 1 ? X + N : Res) + t;
-        const uint32_t* V = (P == 0 ? Res : X + N) + t;
-        uint32_t x[1][32];
-#pragma unroll
-        for (int e = 0; e < 32; e++) x[0][e] = mont(U[e * C::T], V[e * C::T], p, pinv);
-        r32_inv<LOGN>(x, X, t, twi, p, p2);
-        uint32_t* g = G9 + (3 * P + j) * M;
-#pragma unroll
-        for (int e = 0; e < 16; e++) g[t + e * (N / 32)] = x[0][e];
+      if (phase == 0) {
+        //                 G     ADD    AWS    OWS
+        r32_epilogue<LOGN, true, true, false, true>(X, G9 + 0 * M, agg, t, b + inst * M, t1);  // a^2 + b
+        r32_epilogue<LOGN, true, true, false, true>(X, G9 + 3 * M, agg, t, b + inst * M, t2);  // b^2 + b
+        r32_epilogue<LOGN, true, false, false, true>(X, G9 + 6 * M, agg, t, nullptr, t3);       // a b
+      } else {
+        r32_epilogue<LOGN, true, true, true, false>(X, G9 + 6 * M, agg, t, t3, out + inst * M);  // t1 t2 + t3
       }
     }
-    //                 G     ADD    AWS    OWS
-    r32_epilogue<LOGN, true, true, false, true>(X, G9 + 0 * M, agg, t, bi, t1);       // a^2 + b
-    r32_epilogue<LOGN, true, true, false, true>(X, G9 + 3 * M, agg, t, bi, t2);       // b^2 + b
-    r32_epilogue<LOGN, true, false, false, true>(X, G9 + 6 * M, agg, t, nullptr, t3);  // a b
-    // t1 * t2 + t3
-#pragma unroll 1
-    for (int j = 0; j < kNumPrimes; j++) {
-      const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
-      const uint2* twf = tw + (2 * j + 0) * (N - 1);
-      const uint2* twi = tw + (2 * j + 1) * (N - 1);
-      uint32_t xab[2][32];
-      r32_load<LOGN, true>(xab, t1, t2, t, p2);
-      r32_fwd<LOGN>(xab, X, t, twf, p, p2);
-      uint32_t x[1][32];
-#pragma unroll
-      for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
-      r32_inv<LOGN>(x, X, t, twi, p, p2);
-#pragma unroll
-      for (int e = 0; e < 16; e++) Res[j * M + cswz<16>(t + e * (N / 32))] = x[0][e];
-    }
-    r32_epilogue<LOGN, false, true, true, false>(X, Res, agg, t, t3, out + inst * M);
   }
 }
 
