@@ -213,9 +213,15 @@ __global__ void __launch_bounds__(kLbThreads, 2048 / kLbThreads)
   if (tid < 32) agg[tid] = 2u;  // warps past the CTA's count: the operator's identity (g 0, p 1)
   if (tid == 0) tile_s = atomicAdd(counter, 1u);
   __syncthreads();
-  const uint64_t tile = tile_s;
-  if (tile >= total_tiles) return;
-  const uint32_t lt = (uint32_t)(tile % tiles_per_inst);  // tile index within its instance
+  const uint64_t order = tile_s;
+  if (order >= total_tiles) return;
+  // tiles are taken tile-index-major (tile lt of every instance before tile
+  // lt + 1 of any): a tile's predecessor was taken n_inst tiles earlier, so
+  // with many instances in flight it has usually published its inclusive
+  // carry already and the look-back is one read
+  const uint64_t n_inst = total_tiles / tiles_per_inst;
+  const uint32_t lt = (uint32_t)(order / n_inst);      // tile index within its instance
+  const uint64_t tile = (order % n_inst) * tiles_per_inst + lt;  // instance-major flag / data index
   const uint64_t off = tile * (uint64_t)kLbTile + tid * kLbL;  // instances are contiguous
   uint32_t x[kLbL], y[kLbL], r[kLbL], g, p;
   load_limbs<kLbL>(x, a + off);

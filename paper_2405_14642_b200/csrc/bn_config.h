@@ -17,8 +17,9 @@
 // |                             |         | 2-CTA cluster x 16 limbs (1M) (0.331 / 0.379); 2 = 2 / 4-CTA  |
 // |                             |         | clusters, 8 limbs, direct loads, 2 clusters/SM (0.310/0.336) |
 // | BN_ADD_CL_STAGES            | 2       | cp.async stages of variant 0 (3 measured no faster)          |
-// | BN_ADD_BIG_THREADS          | 1024    | bn_add_big tile = threads x 8 limbs (2^18 bits); 512: 2^22    |
-// |                             |         | 0.561 -> 0.570, 256: -> 0.645 (more tiles, more look-backs)   |
+// | BN_ADD_BIG_THREADS          | 1024    | bn_add_big tile = threads x 8 limbs (2^18 bits); 512 / 256    |
+// |                             |         | threads: more tiles and look-backs, slower (2^22: 0.570 /     |
+// |                             |         | 0.645 vs 0.561 ms, instance-major order)                      |
 // | BN_ADD6_BMIN_MID            | 128     | 6-Add CTA size floor from 32K bits (32K 0.324 -> 0.286)      |
 // | BN_ADD6_L12, BN_ADD6_L13    | 16, 16  | 6-Add limbs/thread at 128K / 256K (L=8 at 256K: 1 CTA/SM,    |
 // |                             |         | 0.555 -> 0.377; L=32 at 128K 0.341 -> 0.474)                  |
