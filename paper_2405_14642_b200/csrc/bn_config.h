@@ -25,6 +25,10 @@
 // |                             |         | 0.555 -> 0.377; L=32 at 128K 0.341 -> 0.474)                  |
 // | classical                   |         |                                                              |
 // | BN_CLASSICAL_TT             | 0       | 0 = per-size CTA target (MulCCfg), else a fixed target       |
+// | BN_CLASSICAL_1024_MAXLOG    | 11      | 1-Mul column-group CTAs target 1024 threads for log2 m in    |
+// |                             |         | [8, this] (8K 2.605 -> 2.516 ... 64K 18.73 -> 17.97; 128K    |
+// |                             |         | loses: 37.5 -> 39.0), 512 above                               |
+// | BN_POLYC_1024_MAXLOG        | 12      | the same for the classical Poly (128K 122.2 -> 112.7)         |
 // | BN_CLASSICAL_1K_TT          | 128     | CTA target of the column-group kernel at 1K (when T1 = 0)    |
 // | BN_CLASSICAL_2K_MINB        | 6       | residency target of the 2K column-group kernel               |
 // | BN_CLASSICAL_T1             | 1       | 1K 1-Mul / wide: one thread per instance (0.470 -> 0.347)    |
@@ -76,6 +80,12 @@
 // ---- classical
 #ifndef BN_CLASSICAL_TT
 #define BN_CLASSICAL_TT 0
+#endif
+#ifndef BN_CLASSICAL_1024_MAXLOG
+#define BN_CLASSICAL_1024_MAXLOG 11
+#endif
+#ifndef BN_POLYC_1024_MAXLOG
+#define BN_POLYC_1024_MAXLOG 12
 #endif
 #ifndef BN_CLASSICAL_1K_TT
 #define BN_CLASSICAL_1K_TT 128

@@ -42,7 +42,14 @@ BN_DEV void mac3(uint32_t& lo, uint32_t& hi, uint32_t& top, uint32_t a, uint32_t
       : "r"(a), "r"(b));
 }
 
-template <int LOGM, int Q_>
+// 1024-thread CTA targets (A/B against 512, ms per paper batch): 1-Mul 8K
+// 2.605 -> 2.516, 16K 5.09 -> 4.98, 32K 9.30 -> 9.20, 64K 18.73 -> 17.97
+// (128K: 37.5 -> 39.0, so it stops there); Poly 32K 31.3 -> 30.5, 64K 60.4 ->
+// 58.2, 128K 122.2 -> 112.7; the wide kernel gains nothing (64K: +9.6%).
+constexpr int mul1_tt(int logm) { return logm >= 8 && logm <= BN_CLASSICAL_1024_MAXLOG ? 1024 : 0; }
+constexpr int polyc_tt(int logm) { return logm >= 8 && logm <= BN_POLYC_1024_MAXLOG ? 1024 : 0; }
+
+template <int LOGM, int Q_, int TTX = 0>
 struct MulCCfg {
   static constexpr int M = 1 << LOGM;
   static constexpr int Q = Q_;
@@ -52,7 +59,8 @@ struct MulCCfg {
   // -8%, Poly -8%; 64 is 28% slower), 256 at 2K (more, smaller CTAs overlap
   // one group's barriers / epilogue with another's convolution: -4% vs 512;
   // 128 is 27% slower), 512 above (256 is 10% slower at 4K)
-  static constexpr int TT = BN_CLASSICAL_TT > 0 ? BN_CLASSICAL_TT : (LOGM == 5 ? BN_CLASSICAL_1K_TT : LOGM == 6 ? 256 : 512);
+  static constexpr int TT = BN_CLASSICAL_TT > 0 ? BN_CLASSICAL_TT
+                            : TTX > 0 ? TTX : (LOGM == 5 ? BN_CLASSICAL_1K_TT : LOGM == 6 ? 256 : 512);
   static constexpr int I = (TT / G) >= 32 ? 32 : ((TT / G) < 1 ? 1 : TT / G);
   static constexpr int SET_T = I * G;                         // threads per instance set
   static constexpr int SETS = SET_T >= TT ? 1 : TT / SET_T;   // sets per CTA
@@ -375,9 +383,9 @@ BN_DEV void resolve_lh(const uint32_t* As, const MulCRoles<C>& ro, bool valid, u
 // five extra IMAD.MOVs on the saturated FMA-heavy pipe, 4-5% slower
 // (A/B on one B200, scripts/ab.sh).
 template <int LOGM, int Q>
-__global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB1)
+__global__ void __launch_bounds__(MulCCfg<LOGM, Q, mul1_tt(LOGM)>::T, MulCCfg<LOGM, Q, mul1_tt(LOGM)>::MINB1)
     mul_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
-  using C = MulCCfg<LOGM, Q>;
+  using C = MulCCfg<LOGM, Q, mul1_tt(LOGM)>;
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* agg = sm + 2 * C::STAGE_WORDS;  // T/32
@@ -522,10 +530,10 @@ BN_DEV void classical_phase(uint32_t* As, uint32_t* agg, const MulCRoles<C>& ro,
 }
 
 template <int LOGM, int Q>
-__global__ void __launch_bounds__(MulCCfg<LOGM, Q>::T, MulCCfg<LOGM, Q>::MINB)
+__global__ void __launch_bounds__(MulCCfg<LOGM, Q, polyc_tt(LOGM)>::T, MulCCfg<LOGM, Q, polyc_tt(LOGM)>::MINB)
     poly_classical_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                           uint32_t* ws) {
-  using C = MulCCfg<LOGM, Q>;
+  using C = MulCCfg<LOGM, Q, polyc_tt(LOGM)>;
   constexpr int M = C::M;
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* agg = sm + C::STAGE_WORDS;  // T/32
@@ -693,7 +701,7 @@ template <int LOGM>
 static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                  cudaStream_t st, int n_sm) {
   constexpr int Q = 4;
-  using C = MulCCfg<LOGM, Q>;
+  using C = MulCCfg<LOGM, Q, mul1_tt(LOGM)>;
   constexpr size_t smem = C::SMEM_WORDS * sizeof(uint32_t);
   static LaunchCache cache;
   int per_sm = 0;
@@ -711,7 +719,7 @@ static cudaError_t launch_mulc_t(uint32_t* out, const uint32_t* a, const uint32_
 template <int LOGM>
 static cudaError_t poly_geom_t(uint64_t n_inst, int n_sm, unsigned* grid, uint64_t* ws_words) {
   constexpr int Q = 4;
-  using C = MulCCfg<LOGM, Q>;
+  using C = MulCCfg<LOGM, Q, polyc_tt(LOGM)>;
   constexpr size_t smem = (C::STAGE_WORDS + C::T / 32) * sizeof(uint32_t);
   static LaunchCache cache;
   int per_sm = 0;
@@ -729,7 +737,7 @@ template <int LOGM>
 static cudaError_t launch_polyc_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                                   uint32_t* ws, uint64_t ws_words, cudaStream_t st, int n_sm) {
   constexpr int Q = 4;
-  using C = MulCCfg<LOGM, Q>;
+  using C = MulCCfg<LOGM, Q, polyc_tt(LOGM)>;
   unsigned grid = 0;
   uint64_t need = 0;
   cudaError_t e = poly_geom_t<LOGM>(n_inst, n_sm, &grid, &need);
