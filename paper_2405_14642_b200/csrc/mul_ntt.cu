@@ -1519,16 +1519,22 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 1)
       const uint32_t p = c_pc[j].p, p2 = c_pc[j].p2, pinv = c_pc[j].pinv;
       const uint2* twf = tw + (2 * j + 0) * (N - 1);
       const uint2* twi = tw + (2 * j + 1) * (N - 1);
+      // a, then b, through ONE inlined copy of the forward transform (two
+      // copies spilled more: ptxas -v); A-hat is kept while b is transformed
       uint32_t xa[1][32], xb[1][32];
+#pragma unroll 1
+      for (int v = 0; v < 2; v++) {
+        const uint32_t* src = v ? bi : ai;
 #pragma unroll
-      for (int e = 0; e < 16; e++) {
-        xa[0][e] = red2(red2(__ldg(ai + t + e * (N / 32)), p2), p2);
-        xb[0][e] = red2(red2(__ldg(bi + t + e * (N / 32)), p2), p2);
+        for (int e = 0; e < 16; e++) xb[0][e] = red2(red2(__ldg(src + t + e * (N / 32)), p2), p2);
+#pragma unroll
+        for (int e = 16; e < 32; e++) xb[0][e] = 0u;
+        r32_fwd1<LOGN>(xb, P0, t, twf, p, p2);
+        if (v == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; e++) xa[0][e] = xb[0][e];
+        }
       }
-#pragma unroll
-      for (int e = 16; e < 32; e++) xa[0][e] = xb[0][e] = 0u;
-      r32_fwd1<LOGN>(xa, P0, t, twf, p, p2);
-      r32_fwd1<LOGN>(xb, P0, t, twf, p, p2);
 #pragma unroll
       for (int e = 0; e < 32; e++) xa[0][e] = mont(xa[0][e], xb[0][e], p, pinv);
       r32_inv<LOGN>(xa, P0, t, twi, p, p2);

@@ -25,7 +25,8 @@ CAPTURES = {  # tag -> op@bits
     "ntt_4k": "mul_ntt@4096", "classical_4k": "mul_classical@4096", "add_4k": "add@4096",
     "ntt_128k": "mul_ntt@131072", "ntt_256k": "mul_ntt@262144", "add6_128k": "add6@131072",
     "add6_256k": "add6@262144", "polyntt_4k": "poly_ntt@4096", "polyntt_256k": "poly_ntt@262144",
-    "widentt_256k": "mul_wide_ntt@262144",
+    "widentt_256k": "mul_wide_ntt@262144", "addbig_64m": "add_big@67108864",
+    "classical_64k": "mul_classical@65536",
 }
 
 

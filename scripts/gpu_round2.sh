@@ -23,7 +23,7 @@ prof() {  # tag op bits kernel_regex
   gzip -f gpurun_out/src_$1.csv
   rm -f gpurun_out/prof_$1.ncu-rep
 }
-SPECS=${PROF_SPECS:-"ntt_4k mul_ntt 4096 ^mul_ntt_kernel;classical_4k mul_classical 4096 ^mul_classical_kernel;add_4k add 4096 ^add_kernel;ntt_128k mul_ntt 131072 ^mul_ntt_r32;ntt_256k mul_ntt 262144 ^mul_ntt_r32;add6_128k add6 131072 ^add6;add6_256k add6 262144 ^add6;polyntt_4k poly_ntt 4096 ^poly_ntt;polyntt_256k poly_ntt 262144 ^poly_ntt;widentt_256k mul_wide_ntt 262144 ^mul_wide_ntt"}
+SPECS=${PROF_SPECS:-"ntt_4k mul_ntt 4096 ^mul_ntt_kernel;classical_4k mul_classical 4096 ^mul_classical_kernel;add_4k add 4096 ^add_kernel;ntt_128k mul_ntt 131072 ^mul_ntt_r32;ntt_256k mul_ntt 262144 ^mul_ntt_r32;add6_128k add6 131072 ^add6;add6_256k add6 262144 ^add6;polyntt_4k poly_ntt 4096 ^poly_ntt;polyntt_256k poly_ntt 262144 ^poly_ntt;widentt_256k mul_wide_ntt 262144 ^mul_wide_ntt;addbig_64m add_big 67108864 ^add_lookback;classical_64k mul_classical 65536 ^mul_classical_kernel"}
 IFS=';' read -ra SPEC_LIST <<< "$SPECS"
 for spec in "${SPEC_LIST[@]}"; do prof $spec; done
 if [ "${SANITIZE:-1}" = 1 ]; then
