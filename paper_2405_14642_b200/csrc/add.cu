@@ -15,6 +15,8 @@
 // tail effects.  HBM-bound: 3 * bits / 8 algorithmic bytes per instance
 // (PAPER.md:929).
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "bn_common.cuh"
 #include "bn_kernels.h"
@@ -104,6 +106,166 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
     if (valid) store_limbs<L>(out + off, r);
     if constexpr (C::TPI > 32) __syncthreads();
   }
+}
+
+// ------------------------------------------------- 6-Add with a TMA prefetch
+// From 64K bits (BN_ADD6_TMA_MIN) the register-resident add6_kernel leaves
+// HBM idle: registers (a, b, r: 3 words per limb) hold only two 256K (four
+// 128K) instances per SM, each CTA loads its instance, then runs six
+// dependent CTA scans, and the loads of all CTAs bunch up (ncu r02 at 256K:
+// 35% of the stall samples in load + first scan, long scoreboard).  Here
+// every CTA is persistent and owns ONE instance-sized shared stage (a | b,
+// 2 m words, 64 KiB at 256K): thread 0 fills it with two tensor bulk copies
+// (cp.async.bulk.tensor.2d; the operands viewed as [rows][32 words], one box
+// = one instance, 128-byte swizzle so the 16-limbs-per-thread reads are
+// bank-conflict free) completing on an mbarrier; the threads copy their
+// limbs into registers, and as soon as the first addition's CTA scan has
+// passed its barrier (every thread has read the stage) thread 0 refills the
+// stage with the CTA's NEXT instance, which then lands while the remaining
+// five scans and the store of this one run.  The round-1/2 one-CTA-per-SM
+// ring (three stages, re-reading a, b from shared memory) serialised the six
+// scans at 0.41 ms; here the residency stays register-bound (2 / 4 / 8 CTAs
+// per SM at 256K / 128K / 64K) and only the loads move off the critical path.
+BN_DEV uint32_t mbar_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+BN_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar_addr(bar)), "r"(count) : "memory");
+}
+BN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_addr(bar)), "r"(bytes)
+               : "memory");
+}
+BN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(mbar_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+BN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          mbar_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(mbar_addr(bar))
+      : "memory");
+}
+// 128-byte swizzle of a TMA box (1024-byte aligned): 16-byte chunk c of row r
+// sits at chunk c ^ (r & 7).  Thread lt's 16 limbs are half of row lt / 2,
+// chunks 4 (lt & 1) .. +3: the 8 lanes of a quarter-warp then hit 8
+// distinct chunks of 4 different rows — conflict free.
+template <int L>
+BN_DEV void lds_swz128(uint32_t (&x)[L], const uint32_t* stage, int lt) {
+  static_assert(L == 16, "16 limbs per thread");
+  const int row = lt >> 1, c0 = (lt & 1) * 4;
+#pragma unroll
+  for (int v = 0; v < 4; v++) {
+    const uint4 t = *reinterpret_cast<const uint4*>(stage + row * 32 + 4 * ((c0 + v) ^ (row & 7)));
+    x[4 * v] = t.x;
+    x[4 * v + 1] = t.y;
+    x[4 * v + 2] = t.z;
+    x[4 * v + 3] = t.w;
+  }
+}
+
+template <int LOGM>
+struct Add6TmaCfg {
+  static constexpr int M = 1 << LOGM, L = 16, T = M / L, ROWS = M / 32;
+  static constexpr size_t SMEM = 2 * (size_t)M * 4 + 1024;  // a | b stage + alignment slack
+  static_assert(ROWS <= 256, "one TMA box per operand (box rows <= 256)");
+  static_assert(T >= 64, "the first scan must contain a CTA barrier");
+};
+
+template <int LOGM>
+__global__ void __launch_bounds__(Add6TmaCfg<LOGM>::T, 1024 / Add6TmaCfg<LOGM>::T)
+    add6_tma_kernel(uint32_t* out, const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b, uint64_t n_inst) {
+  using C = Add6TmaCfg<LOGM>;
+  constexpr int M = C::M, L = C::L, T = C::T;
+  extern __shared__ uint8_t smem_raw[];
+  uint32_t* As = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint32_t* Bs = As + M;
+  __shared__ __align__(8) uint64_t full;
+  __shared__ uint32_t agg[2][T / 32];
+  const int lt = threadIdx.x;
+  auto issue = [&](uint64_t inst) {  // thread 0
+    mbar_expect_tx(&full, 2 * M * 4);
+    tma_load_2d(As, &map_a, 0, (int)(inst * C::ROWS), &full);
+    tma_load_2d(Bs, &map_b, 0, (int)(inst * C::ROWS), &full);
+  };
+  if (lt == 0) {
+    mbar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (lt == 0 && blockIdx.x < n_inst) issue(blockIdx.x);
+  uint32_t phase = 0;
+  for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x, phase ^= 1) {
+    mbar_wait(&full, phase);
+    uint32_t x[L], y[L], r[L];
+    lds_swz128<L>(x, As, lt);
+    lds_swz128<L>(y, Bs, lt);
+    uint32_t g, p, cin;
+    chunk_sum<L>(x, y, r, g, p);  // a + b
+    cin = carry_scan<T>(g, p, agg[0]);
+    // carry_scan's CTA barrier: every thread has read the stage -> refill it
+    if (lt == 0 && inst + gridDim.x < n_inst) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(inst + gridDim.x);
+    }
+    add_pending<L, T>(r, x, cin, p, true, agg[1]);  // + a
+    add_pending<L, T>(r, y, cin, p, true, agg[0]);  // + b
+    add_pending<L, T>(r, x, cin, p, true, agg[1]);  // + a
+    add_pending<L, T>(r, y, cin, p, true, agg[0]);  // + b
+    add_pending<L, T>(r, x, cin, p, true, agg[1]);  // + a
+    chunk_apply<L>(x, r, cin);
+    store_limbs<L>(out + inst * (uint64_t)M + lt * L, r);
+    // the next instance's first scan writes agg[0]: its last readers (the
+    // fifth scan) are ordered before the sixth scan's barrier
+  }
+}
+
+// host: a [rows][32 words] view of one operand (rows = n_inst * m / 32), box
+// 32 words x m / 32 rows (one instance), 128-byte swizzle
+static cudaError_t add6_tensor_map(CUtensorMap* map, const uint32_t* base, uint64_t rows, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {32, rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int LOGM>
+static cudaError_t launch_add6_tma_t(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
+                                     cudaStream_t st, int n_sm) {
+  using C = Add6TmaCfg<LOGM>;
+  const uint64_t rows = n_inst * (uint64_t)C::M / 32;
+  if (rows >= (1ull << 31)) return cudaErrorInvalidValue;  // TMA coordinates are int32
+  CUtensorMap ma, mb;
+  cudaError_t e = add6_tensor_map(&ma, a, rows, C::ROWS);
+  if (e != cudaSuccess) return e;
+  e = add6_tensor_map(&mb, b, rows, C::ROWS);
+  if (e != cudaSuccess) return e;
+  static LaunchCache cache;
+  int per_sm = 0;
+  e = resident_ctas(cache, add6_tma_kernel<LOGM>, C::T, C::SMEM, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t cap = (uint64_t)n_sm * per_sm;  // persistent: one resident wave
+  const unsigned grid = cap_grid((unsigned)(n_inst < cap ? n_inst : cap));
+  add6_tma_kernel<LOGM><<<grid, C::T, C::SMEM, st>>>(out, ma, mb, n_inst);
+  return cudaGetLastError();
 }
 
 // Sizes beyond one CTA (2^19, 2^20 bits): one instance per
@@ -403,6 +565,15 @@ cudaError_t launch_add(int logm, uint32_t* out, const uint32_t* a, const uint32_
 
 cudaError_t launch_add6(int logm, uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst,
                         cudaStream_t st, int n_sm) {
+  if (logm >= BN_ADD6_TMA_MIN) {
+    switch (logm) {
+      case 10: return launch_add6_tma_t<10>(out, a, b, n_inst, st, n_sm);
+      case 11: return launch_add6_tma_t<11>(out, a, b, n_inst, st, n_sm);
+      case 12: return launch_add6_tma_t<12>(out, a, b, n_inst, st, n_sm);
+      case 13: return launch_add6_tma_t<13>(out, a, b, n_inst, st, n_sm);
+      default: break;
+    }
+  }
   switch (logm) {
     case 5: return launch_add6_t<5>(out, a, b, n_inst, st, n_sm);
     case 6: return launch_add6_t<6>(out, a, b, n_inst, st, n_sm);

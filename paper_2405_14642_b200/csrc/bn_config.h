@@ -23,6 +23,11 @@
 // | BN_ADD6_BMIN_MID            | 128     | 6-Add CTA size floor from 32K bits (32K 0.324 -> 0.286)      |
 // | BN_ADD6_L12, BN_ADD6_L13    | 16, 16  | 6-Add limbs/thread at 128K / 256K (L=8 at 256K: 1 CTA/SM,    |
 // |                             |         | 0.555 -> 0.377; L=32 at 128K 0.341 -> 0.474)                  |
+// | BN_ADD6_TMA_MIN             | 11      | 6-Add from 2^this limbs (64K bits) through the TMA-prefetch   |
+// |                             |         | kernel (one shared stage per persistent CTA, refilled with    |
+// |                             |         | the next instance after the first scan): 64K 0.290 -> 0.273, |
+// |                             |         | 128K 0.341 -> 0.279, 256K 0.377 -> 0.295; 32K loses (0.273 -> |
+// |                             |         | 0.291), so it keeps the register kernel                       |
 // | classical                   |         |                                                              |
 // | BN_CLASSICAL_TT             | 0       | 0 = per-size CTA target (MulCCfg), else a fixed target       |
 // | BN_CLASSICAL_1024_MAXLOG    | 11      | 1-Mul column-group CTAs target 1024 threads for log2 m in    |
@@ -72,6 +77,9 @@
 #endif
 #ifndef BN_ADD6_L12
 #define BN_ADD6_L12 16
+#endif
+#ifndef BN_ADD6_TMA_MIN
+#define BN_ADD6_TMA_MIN 11
 #endif
 #ifndef BN_ADD6_L13
 #define BN_ADD6_L13 16

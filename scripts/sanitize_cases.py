@@ -1,7 +1,9 @@
 """Small invocations of every kernel for compute-sanitizer (memcheck /
 racecheck / synccheck / initcheck): every op at small and large sizes up to
 its maximum (fused and wide products to 256K bits), ragged batches, a grid
-cap so the persistent paths run, and (--big) the cluster sizes 512K / 1M.  Results are checked against the oracle (any mismatch exits 1)."""
+cap so the persistent paths run, and (--big) the cluster sizes 512K / 1M.  Results are checked against the oracle (any mismatch exits 1).
+SAN_OPS=key[,key] restricts the run to those result keys (add, mul, add6,
+poly, wide)."""
 import os
 import sys
 
@@ -42,7 +44,10 @@ for cap in (0, 2):
                     ("wide", bn.mul_wide_classical), ("wide", bn.mul_wide_ntt)]
         if bits >= (1 << 18):
             ops += [("add", bn.add_big)]
+        only = os.environ.get("SAN_OPS")  # e.g. SAN_OPS=add6: one op key only
         for key, f in ops:
+            if only and key not in only.split(","):
+                continue
             got = inputs.to_numpy_u32(f(da, db))
             torch.cuda.synchronize()
             if not np.array_equal(got, want[key]):

@@ -553,6 +553,35 @@ def test_in_place_fused(bits):
         assert np.array_equal(inputs.to_numpy_u32(da), ref(an, an)), name + " a=b=out"
 
 
+@pytest.mark.parametrize("bits", [65536, 131072, 262144])
+@pytest.mark.parametrize("cap", [1, 3])
+def test_add6_prefetch_grid_cap(bits, cap):
+    """The TMA-prefetch 6-Add (64K bits and up: one shared stage per
+    persistent CTA, refilled with the CTA's next instance after the first
+    scan) with CTAs that run several instances (grid cap), ragged n, RIPPLE
+    operands (carries through every chunk), and in place (out == a, out == b):
+    bit-exact vs the oracle."""
+    m = bits // 32
+    n = 7
+    a, b = inputs.make_operands(n, m, seed=60 + cap, cls="MIX")
+    an, bnp = inputs.to_numpy_u32(a), inputs.to_numpy_u32(b)
+    r, s = inputs.make_operands(n, m, seed=61, cls="RIPPLE")
+    rn, sn = inputs.to_numpy_u32(r), inputs.to_numpy_u32(s)
+    bn.debug_set_grid_cap(cap)
+    try:
+        da, db = a.to(DEV), b.to(DEV)
+        assert np.array_equal(inputs.to_numpy_u32(bn.add6(da, db)), O.add6(an, bnp))
+        dr, ds = r.to(DEV), s.to(DEV)
+        assert np.array_equal(inputs.to_numpy_u32(bn.add6(dr, ds)), O.add6(rn, sn))
+        bn.add6(da, db, out=da)
+        assert np.array_equal(inputs.to_numpy_u32(da), O.add6(an, bnp)), "out=a"
+        da = a.to(DEV)
+        bn.add6(da, db, out=db)
+        assert np.array_equal(inputs.to_numpy_u32(db), O.add6(an, bnp)), "out=b"
+    finally:
+        bn.debug_set_grid_cap(0)
+
+
 @pytest.mark.parametrize("cap", [1, 3])
 def test_wide_ntt_256k_grid_cap(cap):
     """The 256K wide NTT kernel (one 512-thread CTA per instance, incremental
