@@ -154,12 +154,14 @@ BN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint6
 // sits at chunk c ^ (r & 7).  Thread lt's 16 limbs are half of row lt / 2,
 // chunks 4 (lt & 1) .. +3: the 8 lanes of a quarter-warp then hit 8
 // distinct chunks of 4 different rows — conflict free.
+// With L = 32 a thread owns row lt (chunks 0..7): again 8 distinct chunks
+// per quarter-warp step.
 template <int L>
 BN_DEV void lds_swz128(uint32_t (&x)[L], const uint32_t* stage, int lt) {
-  static_assert(L == 16, "16 limbs per thread");
-  const int row = lt >> 1, c0 = (lt & 1) * 4;
+  static_assert(L == 16 || L == 32, "16 or 32 limbs per thread");
+  const int row = L == 16 ? lt >> 1 : lt, c0 = L == 16 ? (lt & 1) * 4 : 0;
 #pragma unroll
-  for (int v = 0; v < 4; v++) {
+  for (int v = 0; v < L / 4; v++) {
     const uint4 t = *reinterpret_cast<const uint4*>(stage + row * 32 + 4 * ((c0 + v) ^ (row & 7)));
     x[4 * v] = t.x;
     x[4 * v + 1] = t.y;
@@ -170,20 +172,23 @@ BN_DEV void lds_swz128(uint32_t (&x)[L], const uint32_t* stage, int lt) {
 
 template <int LOGM>
 struct Add6TmaCfg {
-  static constexpr int M = 1 << LOGM, L = 16, T = M / L, ROWS = M / 32;
+  static constexpr int M = 1 << LOGM, L = LOGM >= BN_ADD6_TMA_L32 ? 32 : 16, T = M / L, ROWS = M / 32;
+  static constexpr int MINB = (L == 32 ? 512 : 1024) / T;  // 128 / 64 registers
   static constexpr size_t SMEM = 2 * (size_t)M * 4 + 1024;  // a | b stage + alignment slack
   static_assert(ROWS <= 256, "one TMA box per operand (box rows <= 256)");
   static_assert(T >= 64, "the first scan must contain a CTA barrier");
 };
 
 template <int LOGM>
-__global__ void __launch_bounds__(Add6TmaCfg<LOGM>::T, 1024 / Add6TmaCfg<LOGM>::T)
+__global__ void __launch_bounds__(Add6TmaCfg<LOGM>::T, Add6TmaCfg<LOGM>::MINB)
     add6_tma_kernel(uint32_t* out, const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, uint64_t n_inst) {
   using C = Add6TmaCfg<LOGM>;
   constexpr int M = C::M, L = C::L, T = C::T;
   extern __shared__ uint8_t smem_raw[];
-  uint32_t* As = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by an offset from the shared array itself (not by integer casts of
+  // a generic pointer), so the stage reads stay LDS.128, not generic LD
+  uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw + ((1024u - (mbar_addr(smem_raw) & 1023u)) & 1023u));
   uint32_t* Bs = As + M;
   __shared__ __align__(8) uint64_t full;
   __shared__ uint32_t agg[2][T / 32];

@@ -28,6 +28,9 @@
 // |                             |         | the next instance after the first scan): 64K 0.290 -> 0.273, |
 // |                             |         | 128K 0.341 -> 0.279, 256K 0.377 -> 0.295; 32K loses (0.273 -> |
 // |                             |         | 0.291), so it keeps the register kernel                       |
+// | BN_ADD6_TMA_L32             | 13      | TMA 6-Add with 32 limbs (one swizzled row) per thread from    |
+// |                             |         | 2^this limbs: 256K 0.295 -> 0.286 (fewer scan instructions    |
+// |                             |         | per limb); 128K 0.267 -> 0.308, 64K 0.274 -> 0.304 lose       |
 // | classical                   |         |                                                              |
 // | BN_CLASSICAL_TT             | 0       | 0 = per-size CTA target (MulCCfg), else a fixed target       |
 // | BN_CLASSICAL_1024_MAXLOG    | 11      | 1-Mul column-group CTAs target 1024 threads for log2 m in    |
@@ -80,6 +83,9 @@
 #endif
 #ifndef BN_ADD6_TMA_MIN
 #define BN_ADD6_TMA_MIN 11
+#endif
+#ifndef BN_ADD6_TMA_L32
+#define BN_ADD6_TMA_L32 13
 #endif
 #ifndef BN_ADD6_L13
 #define BN_ADD6_L13 16
