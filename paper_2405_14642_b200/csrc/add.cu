@@ -232,15 +232,17 @@ __global__ void __launch_bounds__(Add6TmaCfg<LOGM>::T, Add6TmaCfg<LOGM>::MINB)
 
 // host: a [rows][32 words] view of one operand (rows = n_inst * m / 32), box
 // 32 words x m / 32 rows (one instance), 128-byte swizzle
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess) return nullptr;
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
 static cudaError_t add6_tensor_map(CUtensorMap* map, const uint32_t* base, uint64_t rows, uint32_t box_rows) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+  // driver entry point, resolved once (thread-safe static initialisation)
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (!encode) return cudaErrorNotSupported;
   const cuuint64_t dims[2] = {32, rows};
   const cuuint64_t strides[1] = {128};
   const cuuint32_t box[2] = {32, box_rows};
