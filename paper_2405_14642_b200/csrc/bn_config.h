@@ -61,6 +61,10 @@
 // |                             |         | -> 8.30, 2^20 12.1 -> 11.5)                                   |
 // | BN_POLY_NTT_TT              | 256     | CTA target of the 16-element Poly kernel (64: 1K 9.21 ->     |
 // |                             |         | 10.54, 4K 10.18 -> 11.65; 128: 4K 10.27 vs 9.91)              |
+// | BN_NTT_PAIR_CONV            | 1       | 2^20 bits (cluster32, passes 5+5+5+1): the last forward stage, |
+// |                             |         | the pointwise product and the first inverse stage as 2-point  |
+// |                             |         | cyclic convolutions across lane pairs (shuffles), no pass-3   |
+// |                             |         | layout: 11.68 -> 11.62 ms (parity green)                      |
 // | BN_POLY_R32_MIN             | 13      | log2 N from which Poly runs on the 32-element layout (12:    |
 // |                             |         | 64K 15.94 -> 17.77)                                           |
 #pragma once
@@ -153,6 +157,9 @@
 #endif
 #ifndef BN_POLY_NTT_TT
 #define BN_POLY_NTT_TT 256
+#endif
+#ifndef BN_NTT_PAIR_CONV
+#define BN_NTT_PAIR_CONV 1
 #endif
 #ifndef BN_POLY_R32_MIN
 #define BN_POLY_R32_MIN 13

@@ -1239,6 +1239,32 @@ struct NttCl32Cfg {
   static_assert(PassCfgR<LOGN, 1, 5>::LO <= LT, "rank bits on top from pass 1 on");
 };
 
+// The last forward DIF stage and the first inverse DIT stage (stage
+// log2 N - 1: index pairs (i, i ^ 1)) have twiddle 1, so together with the
+// pointwise product between them they are a 2-point cyclic convolution of
+// each pair: with A' = (a0 + a1, a0 - a1), B' likewise, C' = A' B'
+// (Montgomery) and c = (C'0 + C'1, C'0 - C'1):  c0 = S + D, c1 = S - D,
+// S = (a0 + a1)(b0 + b1), D = (a0 - a1)(b0 - b1) — the same lazy-reduced
+// operations in the same order as fwd_pass / mont / inv_pass on that stage.
+// In a layout whose lowest register-free index bit is bit 0 (LO = 1) the
+// partner of every element sits in lane ^ 1, so one shuffle per value
+// replaces the exchange into and out of the bit-0 layout.  Lane bit 0 = 0
+// keeps c0, lane bit 0 = 1 keeps c1.
+BN_DEV void pair_conv_shfl(const uint32_t (&xab)[2][32], uint32_t (&x)[32], uint32_t p, uint32_t p2,
+                           uint32_t pinv) {
+  const bool hi = threadIdx.x & 1;
+#pragma unroll
+  for (int e = 0; e < 32; e++) {
+    const uint32_t ao = __shfl_xor_sync(0xFFFFFFFFu, xab[0][e], 1);
+    const uint32_t bo = __shfl_xor_sync(0xFFFFFFFFu, xab[1][e], 1);
+    const uint32_t a0 = hi ? ao : xab[0][e], a1 = hi ? xab[0][e] : ao;
+    const uint32_t b0 = hi ? bo : xab[1][e], b1 = hi ? xab[1][e] : bo;
+    const uint32_t S = mont(red2(a0 + a1, p2), red2(b0 + b1, p2), p, pinv);
+    const uint32_t D = mont(red2(a0 - a1 + p2, p2), red2(b0 - b1 + p2, p2), p, pinv);
+    x[e] = hi ? S - D + p2 : S + D;
+  }
+}
+
 template <int LO>
 BN_DEV int unlay32_t(int u) { return (u & ((1 << LO) - 1)) | ((u >> (LO + 5)) << LO); }
 
@@ -1303,16 +1329,23 @@ __global__ void __launch_bounds__(512, 1)
       fwd_pass<LOGN, 1, true, 2, 32>(xab, gt, twf, p, p2);
       xchg32<L1, L2, 2, PL>(xab, X0, tid);
       fwd_pass<LOGN, 2, true, 2, 32>(xab, gt, twf, p, p2);
-      if constexpr (C::NP > 3) {
-        xchg32<L2, L3, 2, PL>(xab, X0, tid);
-        fwd_pass<LOGN, 3, true, 2, 32>(xab, gt, twf, p, p2);
-      }
       uint32_t x[1][32];
+      if constexpr (C::NP > 3 && BN_NTT_PAIR_CONV) {
+        // 2^16: the one-stage pass 3 (bit 0) collapses into a 2-point
+        // convolution across lane pairs (pair_conv_shfl): no pass-3 layout,
+        // two exchanges fewer per prime
+        pair_conv_shfl(xab, x[0], p, p2, pinv);
+      } else {
+        if constexpr (C::NP > 3) {
+          xchg32<L2, L3, 2, PL>(xab, X0, tid);
+          fwd_pass<LOGN, 3, true, 2, 32>(xab, gt, twf, p, p2);
+        }
 #pragma unroll
-      for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
-      if constexpr (C::NP > 3) {
-        inv_pass<LOGN, 3, 32>(x[0], gt, twi, p, p2);
-        xchg32<L3, L2, 1, PL>(x, X0, tid);
+        for (int e = 0; e < 32; e++) x[0][e] = mont(xab[0][e], xab[1][e], p, pinv);
+        if constexpr (C::NP > 3) {
+          inv_pass<LOGN, 3, 32>(x[0], gt, twi, p, p2);
+          xchg32<L3, L2, 1, PL>(x, X0, tid);
+        }
       }
       inv_pass<LOGN, 2, 32>(x[0], gt, twi, p, p2);
       xchg32<L2, L1, 1, PL>(x, X0, tid);
