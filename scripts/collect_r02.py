@@ -11,6 +11,7 @@
 Usage: collect_r02.py"""
 import collections
 import csv
+import glob
 import io
 import json
 import os
@@ -26,7 +27,7 @@ CAPTURES = {  # tag -> op@bits
     "ntt_128k": "mul_ntt@131072", "ntt_256k": "mul_ntt@262144", "add6_128k": "add6@131072",
     "add6_256k": "add6@262144", "polyntt_4k": "poly_ntt@4096", "polyntt_256k": "poly_ntt@262144",
     "widentt_256k": "mul_wide_ntt@262144", "addbig_64m": "add_big@67108864",
-    "classical_64k": "mul_classical@65536",
+    "classical_64k": "mul_classical@65536", "ntt_512k": "mul_ntt@524288", "ntt_1m": "mul_ntt@1048576",
 }
 
 
@@ -38,7 +39,8 @@ def main():
     tail = open(os.path.join(G, "pytest_gpu.log")).read().splitlines()[-3:]
     with open(os.path.join(P, "r02_pytest_gpu.log"), "w") as f:
         f.write("python -m pytest tests -m gpu -q (B200, gpurun)\n" + "\n".join(tail) + "\n")
-    shutil.copy(os.path.join(G, "sanitizer.log"), os.path.join(P, "r02_sanitizer.log"))
+    if os.path.exists(os.path.join(G, "sanitizer.log")):  # compute-sanitizer may be closed on the pool
+        shutil.copy(os.path.join(G, "sanitizer.log"), os.path.join(P, "r02_sanitizer.log"))
     # launch list of the bench step
     raw = open(os.path.join(G, "launches.csv")).read()
     body = raw[raw.index('"ID"'):]
@@ -74,6 +76,12 @@ def main():
     kj = os.path.join(P, "ncu_kernels.json")
     if os.path.exists(kj):
         os.remove(kj)
+    # per-size counters first (profiles/r02/ncu_sizes, scripts/gpu_ncu_sizes.sh), then the full
+    # captures, which take precedence where both exist
+    sizes = sorted(glob.glob(os.path.join(P, "r02", "ncu_sizes", "m_*.csv")))
+    if sizes:
+        subprocess.check_call([sys.executable, os.path.join(ROOT, "tools", "ncu_metrics_json.py"), kj] + sizes)
+    specs = [sp for sp in specs if os.path.exists(sp.split(":", 1)[1])]
     subprocess.check_call([sys.executable, os.path.join(ROOT, "tools", "ncu_kernels_json.py"), kj] + specs)
     print(json.dumps(summ, indent=1))
 

@@ -9,7 +9,7 @@ timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo sm
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 tail -1 gpurun_out/pytest_gpu.log
 s0=$(date +%s); timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench_rc=$? wall=$(( $(date +%s) - s0 ))s
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"add_kernel|mul_classical|mul_ntt" -c 24 --csv \
   --log-file gpurun_out/launches.csv python bench.py --no-e2e --no-cpu --no-per-size --steps 5 --warmup 3 \
   > gpurun_out/ncu_launch.log 2>&1; echo launches_rc=$?
 M="--metrics sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"
