@@ -669,7 +669,7 @@ def main():
             raise SystemExit("e2e result differs from the device path")
         line["e2e"] = {"value": 2 * total_inst / dt, "unit": "mults/s", "ms_per_step": dt * 1e3,
                        "h2d_bytes_per_step": 2 * n * m * 4, "d2h_bytes_per_step": 3 * n * m * 4,
-                       "api": "bn_run_host (chunked H2D/compute/D2H on two streams)"}
+                       "api": "bn_run_host (16 MiB chunks, H2D/compute/D2H on three streams)"}
         del ah, bh, outs
     del batches, o_add, o_mc, o_mn
     torch.cuda.empty_cache()

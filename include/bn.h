@@ -191,7 +191,7 @@ bn_status bn_prepare(int device);
  * bn_run_host — runs a sequence of operations over HOST operands: the batch
  * is cut into chunks that are copied host->device, processed by each op in
  * `ops` (same operands a, b), and copied device->host into outs[i], with
- * copies and kernels overlapped on two streams of the current device.
+ * copies and kernels overlapped on three streams of the current device.
  * ops[i] is one of the BN_OP_* codes below (Poly ops get their workspace
  * from the pipeline's own scratch);
  * outs[i] is a host buffer of n_inst*n_limbs limbs.  Host buffers should be

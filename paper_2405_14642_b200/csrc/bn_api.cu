@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/bn.h"
+#include "bn_config.h"
 #include "bn_kernels.h"
 
 namespace bn {
@@ -107,7 +108,7 @@ struct DevState {
   uint2* tw_dev = nullptr;
   bn::NttTables tables[bn::kMaxLogN + 1];
   // bn_run_host scratch
-  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaStream_t st[BN_RUN_HOST_STREAMS] = {};
   uint32_t* scratch = nullptr;
   size_t scratch_bytes = 0;
 };
@@ -480,8 +481,8 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   s = current_device(&d);
   if (s != BN_OK) return s;
   const size_t inst_bytes = (size_t)4 << logm;
-  // chunk: ~32 MiB per operand, at least one instance
-  uint64_t chunk = (32ull << 20) / inst_bytes;
+  // chunk: ~BN_RUN_HOST_CHUNK_MB MiB per operand, at least one instance
+  uint64_t chunk = ((uint64_t)BN_RUN_HOST_CHUNK_MB << 20) / inst_bytes;
   if (chunk < 1) chunk = 1;
   if (chunk > n_inst) chunk = n_inst;
   const size_t chunk_bytes = chunk * inst_bytes;
@@ -498,19 +499,20 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   const size_t per_stream = chunk_bytes * (2 + (size_t)n_ops) + ws_bytes;
   std::lock_guard<std::mutex> lk(g_mu);  // scratch is per device, one pipeline at a time
   cudaError_t e;
+  constexpr int NS = BN_RUN_HOST_STREAMS;
   if (!d->st[0]) {
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < NS; i++) {
       e = cudaStreamCreateWithFlags(&d->st[i], cudaStreamNonBlocking);
       if (e != cudaSuccess) return cuda_fail(e);
     }
   }
-  if (d->scratch_bytes < 2 * per_stream) {
+  if (d->scratch_bytes < NS * per_stream) {
     if (d->scratch) cudaFree(d->scratch);
     d->scratch = nullptr;
     d->scratch_bytes = 0;
-    e = cudaMalloc(&d->scratch, 2 * per_stream);
+    e = cudaMalloc(&d->scratch, NS * per_stream);
     if (e != cudaSuccess) return cuda_fail(e);
-    d->scratch_bytes = 2 * per_stream;
+    d->scratch_bytes = NS * per_stream;
   }
   const char* ha = (const char*)a;
   const char* hb = (const char*)b;
@@ -518,7 +520,7 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   // of earlier chunks must not keep writing into the caller's host buffers
   // (or reading this scratch) after the call has returned
   auto fail = [&](bn_status st) {
-    for (int i = 0; i < 2; i++) (void)cudaStreamSynchronize(d->st[i]);
+    for (int i = 0; i < NS; i++) (void)cudaStreamSynchronize(d->st[i]);
     return st;
   };
   auto fail_cuda = [&](cudaError_t err) {
@@ -529,8 +531,8 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   for (uint64_t i0 = 0; i0 < n_inst; i0 += chunk, c++) {
     const uint64_t n = (n_inst - i0) < chunk ? (n_inst - i0) : chunk;
     const size_t bytes = n * inst_bytes;
-    cudaStream_t st = d->st[c & 1];
-    char* base = (char*)d->scratch + (c & 1) * per_stream;
+    cudaStream_t st = d->st[c % NS];
+    char* base = (char*)d->scratch + (c % NS) * per_stream;
     uint32_t* da = (uint32_t*)base;
     uint32_t* db = (uint32_t*)(base + chunk_bytes);
     e = cudaMemcpyAsync(da, ha + i0 * inst_bytes, bytes, cudaMemcpyHostToDevice, st);
@@ -556,7 +558,7 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
       if (e != cudaSuccess) return fail_cuda(e);
     }
   }
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < NS; i++) {
     e = cudaStreamSynchronize(d->st[i]);
     if (e != cudaSuccess) return fail_cuda(e);
   }

@@ -11,6 +11,10 @@
 //
 // | knob                        | shipped | meaning / evidence                                           |
 // |-----------------------------|---------|--------------------------------------------------------------|
+// | bn_run_host                 |         |                                                              |
+// | BN_RUN_HOST_CHUNK_MB,       | 16, 3   | chunk (MiB per operand) and stream count of the host pipeline |
+// | BN_RUN_HOST_STREAMS         |         | (scripts/e2e_probe.py, 4K step, ms): 32 / 2 34.3, 8 / 2 35.6, |
+// |                             |         | 64 / 2 35.1, 16 / 3 32.2, 32 / 3 32.4, 8 / 4 32.6             |
 // | add                         |         |                                                              |
 // | BN_ADD_BIG                  | 2       | 2^19 / 2^20 bits: 0 = 1024-thread clusters, cp.async staging, |
 // |                             |         | 1 CTA/SM (0.402 / 0.490); 1 = one CTA x 16 limbs (512K), a    |
@@ -68,6 +72,14 @@
 // | BN_POLY_R32_MIN             | 13      | log2 N from which Poly runs on the 32-element layout (12:    |
 // |                             |         | 64K 15.94 -> 17.77)                                           |
 #pragma once
+
+// ---- bn_run_host pipeline
+#ifndef BN_RUN_HOST_CHUNK_MB
+#define BN_RUN_HOST_CHUNK_MB 16
+#endif
+#ifndef BN_RUN_HOST_STREAMS
+#define BN_RUN_HOST_STREAMS 3
+#endif
 
 // ---- add
 #ifndef BN_ADD_BIG

@@ -239,7 +239,9 @@ def test_ntt_forward_stage(lg, prime):
 @pytest.mark.parametrize("bits", [1024, 32768])
 def test_run_host_pipeline(bits):
     m = bits // 32
-    n = max(3, (1 << 27) // bits)  # several 32 MiB chunks at small sizes
+    # 64 MiB per operand + a ragged tail: five 16 MiB chunks, so all three
+    # pipeline streams are reused and the last chunk is partial
+    n = (1 << 29) // bits + 7
     a, b = inputs.make_operands(n, m, seed=4, cls="MIX")
     a, b = a.pin_memory(), b.pin_memory()
     outs = bn.run_host(["add", "mul_classical", "mul_ntt"], a, b)
