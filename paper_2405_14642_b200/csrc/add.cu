@@ -126,30 +126,6 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
 // ring (three stages, re-reading a, b from shared memory) serialised the six
 // scans at 0.41 ms; here the residency stays register-bound (2 / 4 / 8 CTAs
 // per SM at 256K / 128K / 64K) and only the loads move off the critical path.
-BN_DEV uint32_t mbar_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-BN_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar_addr(bar)), "r"(count) : "memory");
-}
-BN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_addr(bar)), "r"(bytes)
-               : "memory");
-}
-BN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(mbar_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-BN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          mbar_addr(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(mbar_addr(bar))
-      : "memory");
-}
 // 128-byte swizzle of a TMA box (1024-byte aligned): 16-byte chunk c of row r
 // sits at chunk c ^ (r & 7).  Thread lt's 16 limbs are half of row lt / 2,
 // chunks 4 (lt & 1) .. +3: the 8 lanes of a quarter-warp then hit 8

@@ -20,6 +20,7 @@
 // carry-in is 0 and its top carry-out is dropped).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "bn_config.h"
@@ -130,6 +131,32 @@ BN_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ------------------------------------------------------------- mbarrier / TMA
+// Completion barriers for bulk (TMA) copies into shared memory.
+BN_DEV uint32_t mbar_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+BN_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar_addr(bar)), "r"(count) : "memory");
+}
+BN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_addr(bar)), "r"(bytes)
+               : "memory");
+}
+BN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(mbar_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+BN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          mbar_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(mbar_addr(bar))
+      : "memory");
+}
 // ------------------------------------------------------------- carry scan
 
 // Mask with bit l set for every lane l that is the top lane of a TPI-lane
