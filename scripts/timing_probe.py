@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Does the per_size timing (one event pair per launch, seeds rotated) differ
-from back-to-back launches on one buffer?  Prints ms per launch for the four
-combinations, for a few (op, bits)."""
+"""Timing-protocol probe (not a bench line): per op and size, the mean launch
+time (a) with one event pair around 100 back-to-back launches on one input,
+(b) the same with the three seeds rotated, (c) bench.py's time_op (one event
+pair per launch, seeds rotated).  Usage: timing_probe.py op[,op] bits[,bits]"""
 import json
 import os
 import sys
@@ -9,33 +10,30 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 from paper_2405_14642_b200 import bn, inputs  # noqa: E402
 
-dev = torch.device("cuda:0")
 bn.prepare(0)
-for op, bits in (("add", 4096), ("add6", 16384), ("add6", 32768), ("add6", 262144), ("mul_ntt", 4096)):
+st = torch.cuda.current_stream()
+for bits in [int(x) for x in sys.argv[2].split(",")]:
     m, n = bits // 32, (1 << 32) // bits
-    ab = [inputs.make_operands(n, m, seed=s, cls="U", device=dev) for s in (1, 2, 3)]
+    ab = [inputs.make_operands(n, m, seed=s, cls="U", device=torch.device("cuda:0")) for s in (1, 2, 3)]
     o = torch.empty_like(ab[0][0])
-    f = getattr(bn, op)
-    reps = 60
-    for rot in (False, True):
-        for per_launch in (False, True):
+    for op in sys.argv[1].split(","):
+        fn = getattr(bn, op)
+        f = lambda k, fn=fn: fn(*ab[k % 3], out=o)  # noqa: E731
+        reps = 100 if "classical" not in op else 20
+        res = {"op": op, "bits": bits}
+        for name, rot in (("one_pair", False), ("one_pair_rot", True)):
             for k in range(3):
-                f(*ab[k % 3], out=o)
+                f(k)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
-            evs[0].record()
+            e0.record()
             for k in range(reps):
-                x, y = ab[k % 3] if rot else ab[0]
-                f(x, y, out=o)
-                if per_launch:
-                    evs[k + 1].record()
-            if not per_launch:
-                evs[reps].record()
+                f(k if rot else 0)
+            e1.record()
             torch.cuda.synchronize()
-            ms = evs[0].elapsed_time(evs[reps]) / reps
-            print(json.dumps({"op": op, "bits": bits, "rotate_seeds": rot, "event_per_launch": per_launch,
-                              "ms": round(ms, 4)}), flush=True)
-    del ab, o
-    torch.cuda.empty_cache()
+            res[name] = round(e0.elapsed_time(e1) / reps, 4)
+        res["time_op"] = round(bench.stats(bench.time_op(torch, f, st, per_rep=True))["ms"], 4)
+        print(json.dumps(res), flush=True)
