@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(AddCfg<LOGM, L, BMIN>::BLOCK)
 // ring (three stages, re-reading a, b from shared memory) serialised the six
 // scans at 0.41 ms; here the residency stays register-bound (2 / 4 / 8 CTAs
 // per SM at 256K / 128K / 64K) and only the loads move off the critical path.
+
 // 128-byte swizzle of a TMA box (1024-byte aligned): 16-byte chunk c of row r
 // sits at chunk c ^ (r & 7).  Thread lt's 16 limbs are half of row lt / 2,
 // chunks 4 (lt & 1) .. +3: the 8 lanes of a quarter-warp then hit 8
