@@ -118,14 +118,22 @@ def test_binding_refuses_cpu_tensors(lib):
 
 
 def test_ntt_primes_are_prime_with_roots(lib):
-    """The library's primes: prime (independent Miller-Rabin), 2^14 | p-1, and
-    their product exceeds the largest exact coefficient m (2^32-1)^2, m = 8192
-    (reading R10)."""
+    """The library's primes: prime (independent Miller-Rabin), and their
+    product exceeds the largest exact coefficient m (2^32-1)^2 at the largest
+    size, m = 32768 (reading R10); the kernel models use the same primes."""
     from oracle.ntt_ref import is_prime
     from paper_2405_14642_b200 import bn
     ps = bn.ntt_primes()
     assert all(is_prime(p) for p in ps)
-    assert ps[0] * ps[1] * ps[2] > 8192 * (2**32 - 1) ** 2
+    # the largest size is 2^20 bits: m = 32768 limbs
+    assert ps[0] * ps[1] * ps[2] > 32768 * (2**32 - 1) ** 2
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "test_kernel_models", os.path.join(os.path.dirname(os.path.abspath(__file__)), "test_kernel_models.py"))
+    models = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(models)
+    assert ps == models.PRIMES  # the CPU kernel models use the same set
 
 
 @pytest.mark.parametrize("op", ["bn_poly_classical", "bn_poly_ntt"])

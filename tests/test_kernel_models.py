@@ -89,7 +89,7 @@ def test_classical_model(m, Q):
 
 # ------------------------------------------------------------------------ NTT
 
-PRIMES = [1073479681, 1073643521, 1073692673]  # the library's set (bn_ntt_primes)
+PRIMES = [1070727169, 1071513601, 1073479681]  # the library's set (bn_ntt_primes; test_abi checks)
 
 
 def _prim_root(p):
@@ -296,3 +296,45 @@ def test_square_block_selection(M, Q):
             k = Q * j0 + q
             want = sum(a[i] * a[k - i] for i in range(k + 1))
             assert got.get(k, 0) == want, (M, Q, j0, k)
+
+
+# ---------------------------------------------------------------------------
+# pair_conv_shfl (mul_ntt.cu, 2^20-bit cluster NTT): the last forward DIF
+# stage and the first inverse DIT stage have twiddle 1; with the pointwise
+# Montgomery product between them they are replaced by c0 = S + D,
+# c1 = S - D + 2p with S = mont(a0 + a1, b0 + b1), D = mont(a0 - a1, b0 - b1)
+# (lazy-reduced).  The replacement must be bit-identical to the three steps
+# it removes (fwd stage w = 1 on both vectors, mont, inv stage w = 1) for
+# every input the forward pass can hand over, i.e. all values in [0, 2p).
+
+def _stage_sequence(a0, a1, b0, b1, p):
+    p2 = 2 * p
+    fa0, fa1 = red2((a0 + a1) & MASK, p2), red2((a0 - a1 + p2) & MASK, p2)   # fwd_pass, w^0
+    fb0, fb1 = red2((b0 + b1) & MASK, p2), red2((b0 - b1 + p2) & MASK, p2)
+    c0, c1 = mont(fa0, fb0, p), mont(fa1, fb1, p)                            # pointwise
+    u, v = red2(c0, p2), red2(c1, p2)                                        # inv_pass, w^0
+    return (u + v) & MASK, (u - v + p2) & MASK
+
+
+def _pair_conv(a0, a1, b0, b1, p):
+    p2 = 2 * p
+    S = mont(red2((a0 + a1) & MASK, p2), red2((b0 + b1) & MASK, p2), p)
+    D = mont(red2((a0 - a1 + p2) & MASK, p2), red2((b0 - b1 + p2) & MASK, p2), p)
+    return (S + D) & MASK, (S - D + p2) & MASK
+
+
+def test_pair_conv_equals_stage_sequence():
+    rng = random.Random(20)
+    for p in PRIMES:
+        p2 = 2 * p
+        edge = [0, 1, p - 1, p, p + 1, p2 - 1]
+        vals = [(x, y, z, w) for x in edge for y in edge for z in (0, p2 - 1) for w in (1, p)]
+        vals += [tuple(rng.randrange(p2) for _ in range(4)) for _ in range(4000)]
+        for a0, a1, b0, b1 in vals:
+            got = _pair_conv(a0, a1, b0, b1, p)
+            assert got == _stage_sequence(a0, a1, b0, b1, p)
+            assert max(got) < 4 * p                     # the inverse pass's input bound
+            # and it is the 2-point cyclic convolution, times 2 R^-1 (R = 2^32)
+            rinv = pow(1 << 32, -1, p)
+            assert got[0] % p == 2 * (a0 * b0 + a1 * b1) * rinv % p
+            assert got[1] % p == 2 * (a0 * b1 + a1 * b0) * rinv % p
