@@ -138,9 +138,9 @@ def test_full_size_bench_config_4096():
     _sample_check(a, b, outs, idx)
 
 
-@pytest.mark.parametrize("bits,n", [(32768, 1 << 17), (262144, 1 << 14)])
+@pytest.mark.parametrize("bits,n", [(32768, 1 << 17), (65536, 1 << 16), (131072, 1 << 15), (262144, 1 << 14)])
 def test_full_size_closed_forms(bits, n):
-    """configs[2] / configs[4]: full paper batch (2^32 bits), worst-case all-ones
+    """configs[2] / configs[3] / configs[4]: full paper batch (2^32 bits), worst-case all-ones
     carry chains: (2^B-1)+(2^B-1) = [FFFFFFFE, FF..], (2^B-1)^2 = 1 mod 2^B,
     (2^B-1)+1 = 0, (2^B-1)*1 = 2^B-1 — checked on every instance."""
     m = bits // 32
