@@ -500,10 +500,14 @@ bn_status bn_run_host(const int* ops, void* const* outs, int n_ops, const void* 
   std::lock_guard<std::mutex> lk(g_mu);  // scratch is per device, one pipeline at a time
   cudaError_t e;
   constexpr int NS = BN_RUN_HOST_STREAMS;
-  if (!d->st[0]) {
+  if (!d->st[NS - 1]) {  // all or none: a partial failure leaves no null stream behind
     for (int i = 0; i < NS; i++) {
+      if (d->st[i]) continue;
       e = cudaStreamCreateWithFlags(&d->st[i], cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_fail(e);
+      if (e != cudaSuccess) {
+        d->st[i] = nullptr;
+        return cuda_fail(e);
+      }
     }
   }
   if (d->scratch_bytes < NS * per_stream) {
