@@ -57,6 +57,9 @@
 // | BN_NTT_TT_MAXLOG            | 12      | larger N use 256-thread targets (16K -9.4%, 32K -7.7%)        |
 // | BN_NTT_SMALL_THREADS        | 768     | residency target for N <= 256: 768 -> 2.882 (80 regs),       |
 // |                             |         | 896 -> 2.891, 1024 -> 2.921                                   |
+// | BN_NTT_MID768_MINLOG        | 12      | 16-element kernel, 2^9..2^12 points: 768 threads/SM (80 regs) |
+// |                             |         | from this log2 N, 512 below (A/B: 64K 4.90 -> 4.84; 8K 3.59  |
+// |                             |         | -> 3.67, 16K 3.80 -> 3.83, 32K equal; 1024: +5-8%, spills)    |
 // | BN_NTT_R32_MIN              | 13      | log2 N from which the 32-element kernel runs (128K: 6.45 ->  |
 // |                             |         | 6.23; 256K: 7.37 -> 6.52; it loses at 32K / 64K)              |
 // | BN_NTT_R32_PREFETCH_MAXLOG  | 13      | next prime's limbs prefetched during the inverse up to this  |
@@ -155,6 +158,9 @@
 #endif
 #ifndef BN_NTT_SMALL_THREADS
 #define BN_NTT_SMALL_THREADS 768
+#endif
+#ifndef BN_NTT_MID768_MINLOG
+#define BN_NTT_MID768_MINLOG 12
 #endif
 #ifndef BN_NTT_R32_MIN
 #define BN_NTT_R32_MIN 13

@@ -115,11 +115,14 @@ struct NttCfg {
   static constexpr int XW = LOGN <= 8 ? IPB * N + (IPB * N >> 4) : IPB * N;
   // two exchange planes (A and B are transformed together), raw residues, agg
   static constexpr int SMEM_WORDS = 2 * XW + IPB * (3 * M + (TPI < 32 ? 16 : 0)) + T / 32;
+  // residency (threads per SM) for 2^9 .. 2^12 points: 768 at 2^12 (80
+  // registers; A/B 64K 4.90 -> 4.84 ms), 512 below (768: 8K +2%, 16K +1%)
+  static constexpr int MT = LOGN >= BN_NTT_MID768_MINLOG ? 768 : 512;
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
   // (A/B on B200: best of {3,4} x {2,3} for T = 256; 2 for T = 512; T = 1024
   // must keep 64 registers)
   static constexpr int MINB = LOGN <= 8 ? (BN_NTT_SMALL_THREADS / T > 1 ? BN_NTT_SMALL_THREADS / T : 1)
-                                        : (T <= 256 ? (512 / T > 1 ? 512 / T : 1) : (T == 512 ? 2 : 1));
+                                        : (T <= 256 ? (MT / T > 1 ? MT / T : 1) : (T == 512 ? 2 : 1));
 };
 
 // pass P covers forward stages [S0, S1); its 16 register elements are the
