@@ -60,6 +60,8 @@
 // | BN_NTT_MID768_MINLOG        | 12      | 16-element kernel, 2^9..2^12 points: 768 threads/SM (80 regs) |
 // |                             |         | from this log2 N, 512 below (A/B: 64K 4.90 -> 4.84; 8K 3.59  |
 // |                             |         | -> 3.67, 16K 3.80 -> 3.83, 32K equal; 1024: +5-8%, spills)    |
+// | BN_NTT_WIDE_THREADS         | 768     | wide NTT residency target up to 2^8 points (1K 2.800 ->      |
+// |                             |         | 2.755, 2K 2.966 -> 2.909, 4K 3.233 -> 3.186; <= 128 regs above)|
 // | BN_NTT_R32_MIN              | 13      | log2 N from which the 32-element kernel runs (128K: 6.45 ->  |
 // |                             |         | 6.23; 256K: 7.37 -> 6.52; it loses at 32K / 64K)              |
 // | BN_NTT_R32_PREFETCH_MAXLOG  | 13      | next prime's limbs prefetched during the inverse up to this  |
@@ -161,6 +163,9 @@
 #endif
 #ifndef BN_NTT_MID768_MINLOG
 #define BN_NTT_MID768_MINLOG 12
+#endif
+#ifndef BN_NTT_WIDE_THREADS
+#define BN_NTT_WIDE_THREADS 768
 #endif
 #ifndef BN_NTT_R32_MIN
 #define BN_NTT_R32_MIN 13

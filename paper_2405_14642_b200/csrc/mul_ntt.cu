@@ -1447,7 +1447,14 @@ struct NttWideCfg {
   using B = NttCfg<LOGN>;
   static constexpr int RS = 3 * B::N + (B::TPI < 32 ? 16 : 0);
   static constexpr int SMEM_WORDS = 2 * B::XW + B::IPB * RS + B::T / 32;
-  static constexpr int MINB = LOGN <= 12 ? 2 : 1;  // <= 128 registers
+  // residency: up to 2^8 points a target of BN_NTT_WIDE_THREADS threads per
+  // SM, bounded by what shared memory admits (A/B, ms per paper batch, 768
+  // vs <= 128 registers: 1K 2.800 -> 2.755, 2K 2.966 -> 2.909, 4K 3.233 ->
+  // 3.186; from 2^9 points 80 registers spill and lose: 8K 4.04 -> 4.43)
+  static constexpr int BY_SMEM = (227 * 1024) / (SMEM_WORDS * 4);
+  static constexpr int BY_THR = BN_NTT_WIDE_THREADS / B::T;
+  static constexpr int MINB = LOGN > 8 ? (LOGN <= 12 ? 2 : 1)  // <= 128 registers
+                                       : (BY_THR < 1 ? 1 : (BY_THR < BY_SMEM ? BY_THR : (BY_SMEM < 1 ? 1 : BY_SMEM)));
 };
 
 template <int LOGN>
