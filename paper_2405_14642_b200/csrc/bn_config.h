@@ -55,8 +55,10 @@
 // | BN_NTT_TT                   | 64      | CTA target of the 16-element kernel, N <= 2^BN_NTT_TT_MAXLOG: |
 // |                             |         | 4K 256 -> 2.953, 128 -> 2.879, 64 -> 2.873, 32 -> 2.884       |
 // | BN_NTT_TT_MAXLOG            | 12      | larger N use 256-thread targets (16K -9.4%, 32K -7.7%)        |
-// | BN_NTT_SMALL_THREADS        | 768     | residency target for N <= 256: 768 -> 2.882 (80 regs),       |
-// |                             |         | 896 -> 2.891, 1024 -> 2.921                                   |
+// | BN_NTT_SMALL_THREADS        | 576     | residency target for N <= 256 (registers follow): 4K 768 ->  |
+// |                             |         | 2.882 (80 regs), 896 -> 2.891, 1024 -> 2.921; round 2: 704    |
+// |                             |         | 2.871 (80), 640 2.854 (96), 576 2.833 (96), 512 2.916 (104);  |
+// |                             |         | 576 also 2K 2.572 -> 2.540, 1K 2.318 -> 2.309                 |
 // | BN_NTT_MID768_MINLOG        | 12      | 16-element kernel, 2^9..2^12 points: 768 threads/SM (80 regs) |
 // |                             |         | from this log2 N, 512 below (A/B: 64K 4.90 -> 4.84; 8K 3.59  |
 // |                             |         | -> 3.67, 16K 3.80 -> 3.83, 32K equal; 1024: +5-8%, spills)    |
@@ -159,7 +161,7 @@
 #define BN_NTT_TT_MAXLOG 12
 #endif
 #ifndef BN_NTT_SMALL_THREADS
-#define BN_NTT_SMALL_THREADS 768
+#define BN_NTT_SMALL_THREADS 576
 #endif
 #ifndef BN_NTT_MID768_MINLOG
 #define BN_NTT_MID768_MINLOG 12

@@ -32,23 +32,10 @@
 
 namespace cg = cooperative_groups;
 
-// Cluster NTT geometry.  A/B on B200 (scripts/ab.sh): 1024 threads per CTA
-// (64 registers, some spills) beat 512 threads per CTA at every cluster size
-// (2^18 as a 2 x 512 cluster: 8.76 ms vs 7.37 ms one CTA; 2^19: 10.9 vs 9.6;
-// 2^20: 13.3 vs 12.2), so the defaults are 1024 and one CTA up to 2^18.
-// -DBN_NTT14_CLUSTER -DBN_NTT_CL_T=512 [-DBN_NTT_CL_MINB=1] rebuild the variants.
-// target CTA size of the 16-element kernel for N <= 256 (several instances per CTA)
-// target CTA size of the 16-element Poly kernel
+// Kernel geometry (CTA sizes, residency targets, which layout runs at which
+// size) is one table with its A/B evidence: bn_config.h.
+// CTA target of the 16-element Poly kernel
 constexpr int kPolyNttTT = BN_POLY_NTT_TT;
-// smallest log2 N whose Poly runs on the 32-element layout
-// Poly on the 32-element layout: forward-transform a and b one at a time
-// residency target (threads per SM) of the 16-element kernel for N <= 256.
-// A/B at 4K (ms): 768 -> 2.882 (80 registers), 896 -> 2.891 (72), 1024 ->
-// 2.921 (64; shared memory caps all three at 12-14 CTAs of 64 threads)
-// smallest log2 N that uses the 32-element-per-thread kernel
-// r32 kernel: prefetch the next prime's / instance's raw limbs during the
-// inverse for LOGN <= this (A/B on B200, ms per paper batch: 128K 6.27 ->
-// 6.17; 256K 6.53 -> 6.66, where the 32 extra live registers add spills)
 // Timing-only experiment (never in a shipped build): BN_DBG_TWCONST replaces
 // every twiddle load by a value derived from the pointer (no memory access),
 // to measure what the table loads cost.  Results are WRONG with it.
