@@ -62,6 +62,8 @@
 // | BN_NTT_MID768_MINLOG        | 12      | 16-element kernel, 2^9..2^12 points: 768 threads/SM (80 regs) |
 // |                             |         | from this log2 N, 512 below (A/B: 64K 4.90 -> 4.84; 8K 3.59  |
 // |                             |         | -> 3.67, 16K 3.80 -> 3.83, 32K equal; 1024: +5-8%, spills)    |
+// | BN_NTT_MID9_THREADS         | 640     | the same at 2^9 points (8K bits): 512 3.593, 576 3.641, 640   |
+// |                             |         | 3.536 ms (96 registers); 640 loses at 16K / 32K (+0.3%)       |
 // | BN_NTT_WIDE_THREADS         | 768     | wide NTT residency target up to 2^8 points (1K 2.800 ->      |
 // |                             |         | 2.755, 2K 2.966 -> 2.909, 4K 3.233 -> 3.186; <= 128 regs above)|
 // | BN_NTT_R32_MIN              | 13      | log2 N from which the 32-element kernel runs (128K: 6.45 ->  |
@@ -162,6 +164,9 @@
 #endif
 #ifndef BN_NTT_SMALL_THREADS
 #define BN_NTT_SMALL_THREADS 576
+#endif
+#ifndef BN_NTT_MID9_THREADS
+#define BN_NTT_MID9_THREADS 640
 #endif
 #ifndef BN_NTT_MID768_MINLOG
 #define BN_NTT_MID768_MINLOG 12

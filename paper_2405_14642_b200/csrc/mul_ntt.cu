@@ -102,9 +102,9 @@ struct NttCfg {
   static constexpr int XW = LOGN <= 8 ? IPB * N + (IPB * N >> 4) : IPB * N;
   // two exchange planes (A and B are transformed together), raw residues, agg
   static constexpr int SMEM_WORDS = 2 * XW + IPB * (3 * M + (TPI < 32 ? 16 : 0)) + T / 32;
-  // residency (threads per SM) for 2^9 .. 2^12 points: 768 at 2^12 (80
-  // registers; A/B 64K 4.90 -> 4.84 ms), 512 below (768: 8K +2%, 16K +1%)
-  static constexpr int MT = LOGN >= BN_NTT_MID768_MINLOG ? 768 : 512;
+  // residency (threads per SM) for 2^9 .. 2^12 points (bn_config.h): 768 at
+  // 2^12, BN_NTT_MID9_THREADS at 2^9, 512 between
+  static constexpr int MT = LOGN >= BN_NTT_MID768_MINLOG ? 768 : (LOGN == 9 ? BN_NTT_MID9_THREADS : 512);
   // residency target: 4 CTAs of 256 threads (64 regs) for small N, else 1-2
   // (A/B on B200: best of {3,4} x {2,3} for T = 256; 2 for T = 512; T = 1024
   // must keep 64 registers)
