@@ -40,7 +40,8 @@
 // | BN_CLASSICAL_1024_MAXLOG    | 11      | 1-Mul column-group CTAs target 1024 threads for log2 m in    |
 // |                             |         | [8, this] (8K 2.605 -> 2.516 ... 64K 18.73 -> 17.97; 128K    |
 // |                             |         | loses: 37.5 -> 39.0), 512 above; 4K (log2 m = 7) loses too:   |
-// |                             |         | 1.347 -> 1.447 (round 2)                                      |
+// |                             |         | 1.347 -> 1.447 (round 2); 256-thread CTAs at 4K: 1.485 (64    |
+// |                             |         | regs) / 1.512 (78 regs, 3 per SM); 128 x 3: 1.638             |
 // | BN_POLYC_1024_MAXLOG        | 12      | the same for the classical Poly (128K 122.2 -> 112.7)         |
 // | BN_CLASSICAL_1K_TT          | 128     | CTA target of the column-group kernel at 1K (when T1 = 0)    |
 // | BN_CLASSICAL_2K_MINB        | 6       | residency target of the 2K column-group kernel               |
