@@ -51,7 +51,11 @@
 // | BN_CLASSICAL_T1_MINB        | 5       | 1K residency: 4 -> 0.395, 5 -> 0.389, 6 -> 0.398             |
 // | BN_CLASSICAL_T1_MINB_2K     | 6       | 2K residency: 4 -> 0.612, 6 -> 0.607 (168 registers)         |
 // | BN_POLY_T1_2K               | 1       | 2K Poly one thread per instance (2.685 -> 2.297)             |
-// | BN_POLY_T1_MINB             | 6       | 168 registers, 6 CTAs x 32 KiB per SM                        |
+// | BN_CLASSICAL_T1_MINB_WIDE_2K| 4       | 2K full product residency: 255 registers, no spills: 1.232 -> |
+// |                             |         | 1.215 (6: 168 registers, 48 / 92 bytes of spills; 5: 1.291)   |
+// | BN_POLY_T1_MINB             | 6       | 1K Poly: 168 registers, 6 CTAs x 32 KiB per SM                |
+// | BN_POLY_T1_MINB_2K          | 4       | 2K Poly: 255 registers, no spills: 2.29 -> 2.05 (6: 168 regs, |
+// |                             |         | 64 bytes of spills); at 1K 4 loses (1.036 -> 1.22)            |
 // | NTT                         |         |                                                              |
 // | BN_NTT_TT                   | 64      | CTA target of the 16-element kernel, N <= 2^BN_NTT_TT_MAXLOG: |
 // |                             |         | 4K 256 -> 2.953, 128 -> 2.879, 64 -> 2.873, 32 -> 2.884       |
@@ -151,6 +155,12 @@
 #endif
 #ifndef BN_POLY_T1_2K
 #define BN_POLY_T1_2K 1
+#endif
+#ifndef BN_POLY_T1_MINB_2K
+#define BN_POLY_T1_MINB_2K 4
+#endif
+#ifndef BN_CLASSICAL_T1_MINB_WIDE_2K
+#define BN_CLASSICAL_T1_MINB_WIDE_2K 4
 #endif
 #ifndef BN_POLY_T1_MINB
 #define BN_POLY_T1_MINB 6

@@ -946,7 +946,9 @@ constexpr int kT1Threads = 128;
 // 1-Mul 1 stage 0.348 / 2 stages 0.368, full product 0.697 / 0.635
 constexpr int t1_stages(int m, bool wide) { return m == 32 && wide ? 2 : 1; }
 constexpr int t1_threads(int m, bool wide) { return m == 32 && t1_stages(m, wide) == 1 ? kT1Threads : 64; }
-constexpr int t1_minb(int m, bool wide) { return m == 32 && !wide ? BN_CLASSICAL_T1_MINB : BN_CLASSICAL_T1_MINB_2K; }
+constexpr int t1_minb(int m, bool wide) {
+  return m == 32 && !wide ? BN_CLASSICAL_T1_MINB : (wide && m == 64 ? BN_CLASSICAL_T1_MINB_WIDE_2K : BN_CLASSICAL_T1_MINB_2K);
+}
 // WIDE: all 2M columns (the full product, bn_mul_wide_classical).
 template <int M, bool WIDE>
 __global__ void __launch_bounds__(t1_threads(M, WIDE), t1_minb(M, WIDE))
@@ -1124,7 +1126,7 @@ BN_DEV void t1_prod(const uint32_t (&x)[M], const uint32_t (&y)[M], Add add, Sin
 // overwrite it (each lane its own rows) and the next tile is loaded after
 // the product instead of during it (PF = false).
 template <int M>
-__global__ void __launch_bounds__(kPolyT1Threads, BN_POLY_T1_MINB)
+__global__ void __launch_bounds__(kPolyT1Threads, M == 32 ? BN_POLY_T1_MINB : BN_POLY_T1_MINB_2K)
     poly_classical_t1_kernel(uint32_t* out, const uint32_t* a, const uint32_t* b, uint64_t n_inst) {
   static_assert(M % 32 == 0, "row swizzle assumes a multiple of 8 chunks per row");
   constexpr bool PF = M == 32;
