@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Side-by-side of our B200 sweep (profiles/r01_sweep.jsonl) with the paper's
+"""Side-by-side of our B200 numbers (a bench line's per_size, or the round-1
+sweep profiles/r01_sweep.jsonl) with the paper's
 A100 numbers (BASELINE.md Tables 1-2) —
 context only: other hardware, and the paper's FFT digit scheme is inexact
 (reading R10).  Prints a markdown table."""
@@ -21,8 +22,30 @@ PAPER = {
 }
 
 
+def _from_bench_line(line):
+    """rows of the sweep format from a bench line's per_size block; Poly
+    Gu32ops/s = 4 multiplications x the paper's 1-Mul u32-op count
+    (300 m log2 m) per instance"""
+    import math
+    rows = []
+    for bits, row in line["per_size"].items():
+        if not bits.isdigit():
+            continue
+        b, m = int(bits), int(bits) // 32
+        for op, r in row.items():
+            if not isinstance(r, dict):
+                continue
+            r = dict(r, op=op, bits=b)
+            if op.startswith("poly") and "poly/s" in r:
+                r["Gu32ops/s"] = r["poly/s"] * 4 * 300 * m * math.log2(m) / 1e9
+            rows.append(r)
+    return rows
+
+
 def main(path=os.path.join(ROOT, "profiles", "r01_sweep.jsonl")):
-    rows = [json.loads(l) for l in open(path)]
+    """path: a --sweep JSONL (round 1) or a bench JSON line with per_size"""
+    lines = [json.loads(l) for l in open(path) if l.strip()]
+    rows = _from_bench_line(lines[-1]) if "per_size" in lines[-1] else lines
     by = {}
     for r in rows:
         by.setdefault(r["op"], {})[r["bits"]] = r
