@@ -14,6 +14,7 @@
 // (grid-stride over instance groups) so small sizes amortise launch and
 // tail effects.  HBM-bound: 3 * bits / 8 algorithmic bytes per instance
 // (PAPER.md:929).
+#include <cassert>
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -165,11 +166,16 @@ __global__ void __launch_bounds__(Add6TmaCfg<LOGM>::T, Add6TmaCfg<LOGM>::MINB)
   extern __shared__ uint8_t smem_raw[];
   // align by an offset from the shared array itself (not by integer casts of
   // a generic pointer), so the stage reads stay LDS.128, not generic LD
-  uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw + ((1024u - (mbar_addr(smem_raw) & 1023u)) & 1023u));
+  const uint32_t pad = (1024u - (mbar_addr(smem_raw) & 1023u)) & 1023u;
+  uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw + pad);
   uint32_t* Bs = As + M;
   __shared__ __align__(8) uint64_t full;
   __shared__ uint32_t agg[2][T / 32];
   const int lt = threadIdx.x;
+#ifdef BN_BOUNDS_CHECK  // debug builds (scripts/bounds_check.sh): the aligned stage fits the allocation
+  assert(pad + 2u * M * 4u <= C::SMEM && (mbar_addr(As) & 1023u) == 0 && blockDim.x == T);
+  assert((L == 16 ? lt >> 1 : lt) < M / 32);
+#endif
   auto issue = [&](uint64_t inst) {  // thread 0
     mbar_expect_tx(&full, 2 * M * 4);
     tma_load_2d(As, &map_a, 0, (int)(inst * C::ROWS), &full);
